@@ -1,0 +1,134 @@
+/*
+ * gazecut_b200.h -- C ABI of the B200-native gaze-line stereo graph-cut path.
+ *
+ * Drop-in boundary for the reference package `gazecut` (arXiv 1803.01516).
+ * The reference has no FFI: its boundary is the Python API exported by
+ * pkg/src/gazecut/__init__.py:11-97.  Each entry point below replaces the
+ * reference function named beside it; the Python mirror in
+ * paper_1803_01516_b200/ binds them with ctypes.
+ *
+ * Conventions
+ *  - All array pointers are DEVICE pointers unless the name ends in _host.
+ *  - Calls are ordered on the given stream (a cudaStream_t passed as void*;
+ *    NULL = legacy default stream).  Functions that fill a gz_stats block
+ *    synchronise the stream before returning.
+ *  - Return value: GZ_OK (0) or a negative gz_status.
+ *  - Volumes cross the ABI as int32 in the reference's (rows, cols, m)
+ *    order (energy.py:83-114 returns int64; the Python mirror range-checks
+ *    and narrows on upload).
+ *  - Labelings are int32 (rows, cols), cuboid-local label indices, exactly
+ *    as maxflow.py:362-373 extract_labeling returns them.
+ */
+#ifndef GAZECUT_B200_H
+#define GAZECUT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum gz_status {
+    GZ_OK = 0,
+    GZ_ERR_ARG = -1,          /* ValueError in the reference (bad shape / window / params) */
+    GZ_ERR_CUDA = -2,         /* a CUDA runtime call failed */
+    GZ_ERR_WORKSPACE = -3,    /* workspace smaller than gz_workspace_bytes() */
+    GZ_ERR_CONSISTENCY = -4,  /* InternalConsistencyError (maxflow.py:51-52): cut cost != labeling energy */
+    GZ_ERR_OVERFLOW = -5,     /* capacities too large for the int32 device state */
+    GZ_ERR_NOCONVERGE = -6,   /* internal iteration guard tripped (never expected) */
+    GZ_ERR_NOGPU = -7         /* no sm_100 device */
+};
+
+/* geometry.py:61-138 CuboidSpec (the fields the data term needs) */
+typedef struct {
+    int32_t width, height;     /* image size the cuboid was built for */
+    int32_t g_min, g_extent;
+    int32_t y_min, y_extent;
+    int32_t d_min, m;          /* first depth number, number of labels */
+} gz_cuboid;
+
+/* energy.py:37-50 EnergyParams */
+typedef struct {
+    int32_t penalty, inhibit, hard_inhibit;
+} gz_energy;
+
+/* Solver schedule.  maxflow.py:403-409 maxflow_push_relabel arguments plus
+ * the device schedule knobs.  Zero-initialised = the defaults. */
+typedef struct {
+    int32_t rounds_per_sweep;  /* synchronous push/relabel pulses per sweep (default 12) */
+    int32_t max_sweeps;        /* sweep cap, honoured only with GZ_SCHED_CAPPED (level-2 mode) */
+    int32_t bfs_cap;           /* lateral BFS relaxations per non-final global relabel (0 = exact) */
+    int32_t flags;             /* GZ_SCHED_NO_WAVE: skip the chain wave (maxflow.py:422 presaturate=False);
+                                  GZ_SCHED_CAPPED: stop after max_sweeps sweeps (maxflow.py:447-449) */
+} gz_sched;
+
+#define GZ_SCHED_NO_WAVE 1
+#define GZ_SCHED_CAPPED 2
+
+/* maxflow.py:460-471 + 506-509 stats keys, plus device timings. */
+typedef struct {
+    int64_t flow, energy, const_offset, nodes, arcs, presaturated, pushes, relabels;
+    int64_t labeling_energy;       /* energy.py:129-155 recomputed on device */
+    int32_t sweeps, converged, stranded_excess_nodes, bfs_passes, reach_passes, pulses;
+    float ms_total;                /* device time of the solve (CUDA events) */
+    float ms_reserved[3];
+} gz_stats;
+
+/* Device bytes the caller must provide as workspace for one problem of the
+ * given site grid and label count (batch problems: multiply). */
+size_t gz_workspace_bytes(int32_t rows, int32_t cols, int32_t m);
+
+/* energy.py:83-114 sad_volume.  left/right: uint8 (height, width, channels)
+ * row-major; vol_out: int32 (y_extent, g_extent, m). */
+int gz_sad_volume(const uint8_t *left, const uint8_t *right, int32_t img_h, int32_t img_w,
+                  int32_t channels, const gz_cuboid *cuboid, int32_t *vol_out, void *stream);
+
+/* maxflow.py:481-510 solve_exact (lo == hi == NULL) and
+ * hierarchy.py:76-89 _solve_restricted_exact (per-site windows lo/hi, int32
+ * rows*cols, 0 <= lo <= hi < m).  vol: int32 (rows, cols, m).
+ * labels_out: int32 (rows, cols).  The source side (maxflow.py:355-359) is
+ * the prefix lo+1 .. label of every chain, so it is derived from the labels. */
+int gz_solve_volume(const int32_t *vol, int32_t rows, int32_t cols, int32_t m, const gz_energy *energy,
+                    const gz_sched *sched, const int32_t *lo, const int32_t *hi, int32_t *labels_out,
+                    gz_stats *stats_out, void *workspace, size_t workspace_bytes,
+                    void *stream);
+
+/* Fused path: sad_volume + solve_exact for `batch` stereo pairs laid out
+ * back to back (left/right: batch x height x width x channels uint8).
+ * labels_out: batch x (y_extent, g_extent) int32; stats_out: batch entries
+ * (host memory).  workspace: batch * gz_workspace_bytes(y_extent, g_extent, m). */
+int gz_solve_pairs(const uint8_t *left, const uint8_t *right, int32_t batch, int32_t img_h, int32_t img_w,
+                   int32_t channels, const gz_cuboid *cuboid, const gz_energy *energy, const gz_sched *sched,
+                   int32_t *labels_out, gz_stats *stats_out, void *workspace, size_t workspace_bytes,
+                   void *stream);
+
+/* Same as gz_solve_pairs with HOST buffers (pinned or pageable): copies in,
+ * solves, copies labels out.  The reference-facing end-to-end call. */
+int gz_solve_pairs_host(const uint8_t *left_host, const uint8_t *right_host, int32_t batch, int32_t img_h,
+                        int32_t img_w, int32_t channels, const gz_cuboid *cuboid, const gz_energy *energy,
+                        const gz_sched *sched, int32_t *labels_host, gz_stats *stats_host, void *workspace,
+                        size_t workspace_bytes, void *stream);
+
+/* energy.py:129-155 total_energy on device.  Writes one int64 to energy_out (device). */
+int gz_total_energy(const int32_t *labels, const int32_t *vol, int32_t rows, int32_t cols, int32_t m,
+                    const gz_energy *energy, int64_t *energy_out, void *stream);
+
+/* hierarchy.py:39-57 coarsen: vol (rows, cols, m) -> coarse (ceil(rows/b), ceil(cols/b), ceil(m/b)). */
+int gz_coarsen(const int32_t *vol, int32_t rows, int32_t cols, int32_t m, int32_t block, int32_t *coarse_out,
+               void *stream);
+
+/* hierarchy.py:60-73 thin_skin: coarse labeling (crows, ccols) -> lo/hi (rows, cols). */
+int gz_thin_skin(const int32_t *coarse_labels, int32_t crows, int32_t ccols, int32_t rows, int32_t cols,
+                 int32_t m, int32_t block, int32_t radius, int32_t *lo_out, int32_t *hi_out, void *stream);
+
+/* Human-readable status. */
+const char *gz_status_string(int status);
+
+/* Library/kernel build identification (for provenance). */
+const char *gz_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GAZECUT_B200_H */

@@ -1,0 +1,58 @@
+"""B200-native gaze-line stereo graph cuts (arXiv 1803.01516).
+
+Drop-in for the hot path of the reference package ``gazecut``
+(pkg/src/gazecut/__init__.py:11-97): stereo pair in, per-site depth labels,
+flow and energy out.  The data term, graph initialisation, push-relabel
+max-flow, min-cut read-out, energy check and hierarchy helpers run as
+hand-written sm_100a CUDA kernels in ``libgazecut_b200.so`` behind a C ABI
+(include/gazecut_b200.h).  There is no CPU fallback.
+
+Out of scope: image I/O (imaging.py), accuracy accounting
+(evalreport.py), the CLI and generic CSR networks.
+"""
+
+from .energy import UNCUTTABLE, EnergyParams, pairwise_term, sad_volume, sad_volume_device, total_energy
+from .flownet import (
+    FlowNetwork,
+    build_network,
+    expected_arc_count,
+    expected_node_count,
+    full_windows,
+    network_from_arcs,
+)
+from .geometry import (
+    CuboidSpec,
+    GazeDepthCoord,
+    WhsCoord,
+    cross_from_pixels,
+    cuboid_from_disparity_range,
+    cuboid_with_offsets,
+    disparity_from_whs,
+    pixels_from_gaze_depth,
+    whs_from_disparity,
+)
+from .hierarchy import coarsen, solve_level1, solve_level2, thin_skin
+from .maxflow import (
+    CutResult,
+    InternalConsistencyError,
+    extract_labeling,
+    maxflow_push_relabel,
+    maxflow_reference,
+    solve_exact,
+    source_side,
+)
+from .pairs import PairSolver, solve_pairs
+from .synthetic import SyntheticScene, make_scene
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "CuboidSpec", "CutResult", "EnergyParams", "FlowNetwork", "GazeDepthCoord", "InternalConsistencyError",
+    "PairSolver", "SyntheticScene", "UNCUTTABLE", "WhsCoord", "build_network", "coarsen",
+    "cross_from_pixels", "cuboid_from_disparity_range", "cuboid_with_offsets", "disparity_from_whs",
+    "expected_arc_count", "expected_node_count", "extract_labeling", "full_windows", "make_scene",
+    "maxflow_push_relabel", "maxflow_reference", "network_from_arcs", "pairwise_term",
+    "pixels_from_gaze_depth", "sad_volume", "sad_volume_device", "solve_exact", "solve_level1",
+    "solve_level2", "solve_pairs", "source_side", "thin_skin", "total_energy", "whs_from_disparity",
+    "__version__",
+]

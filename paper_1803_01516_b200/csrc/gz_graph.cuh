@@ -1,0 +1,76 @@
+// gz_graph.cuh -- implicit Ishikawa layered graph on the (level, row, gaze) grid.
+//
+// The reference builds an explicit CSR network (flownet.py:102-222).  Here the
+// graph is never materialised: node (t, c) for chain position t = 1..M-1 of site
+// c = y*G + g lives at flat index t*P + c (P = Y*G, "plane-major"), and the
+// 14 arcs of a node are enumerated by index arithmetic.  Residual state:
+//
+//   cu [k][c]  forward residual of chain arc k (position k -> k+1), k = 0..M-1.
+//              The reverse chain arc is UNCUTTABLE (flownet.py:131) and never
+//              saturates, so it is not stored.
+//   ph [t][c]  residual of the same-level arc (y,g,t)->(y,g+1,t); the reverse
+//              residual is 2*penalty - ph (capacity penalty each way,
+//              flownet.py:147-161).
+//   pv [t][c]  same for (y,g,t)->(y+1,g,t).
+//   dar[t][c]  flow on the inhibit diagonal (y,g,t)->(y,g+1,t-1)   (flownet.py:163-180,
+//   dbr[t][c]  flow on (y,g+1,t)->(y,g,t-1)                         direction 0 / 1,
+//   dad[t][c]  flow on (y,g,t)->(y+1,g,t-1)                         forward capacity
+//   dbd[t][c]  flow on (y+1,g,t)->(y,g,t-1)                         inhibit, reverse 0)
+//
+// Label windows (flownet.py:17-21, 92-99): position t of site c is the source
+// if t <= lo[c], the sink if t > hi[c], a real node otherwise.  Arcs into
+// sink positions are exits to the sink; arcs into source positions are never
+// used (the solver stops after phase 1); arcs out of source
+// positions are saturated at initialisation; source->sink arcs fold into the
+// constant offset exactly as flownet.py:124-125,153-154,172-173 do.
+#pragma once
+#include <cstdint>
+
+namespace gz {
+
+constexpr int32_t HINF = 0x3fffffff;        // "cannot reach the sink"
+// Finite stand-in for UNCUTTABLE inhibit diagonals in hard mode.  A flow that
+// crosses k uncuttable arcs is k*HARD_CAP + f on the device and is reported as
+// k*2^56 + f, the reference's value (exact while f < HARD_CAP).
+constexpr int32_t HARD_CAP = 1 << 27;
+constexpr long long UNCUTTABLE = 1LL << 56; // energy.py:34
+
+// arc slots of a node, in push order
+enum Arc : int {
+    A_UP = 0,      // chain (t -> t+1)
+    A_SR, A_SL, A_SD, A_SU,   // same level  right/left/down/up
+    A_UR, A_UL, A_UD, A_UU,   // diagonal up (t -> t+1) = reverse of neighbour's inhibit diagonal
+    A_DR, A_DL, A_DD, A_DU,   // diagonal down (t -> t-1) = inhibit diagonal
+    A_DN,          // chain (t -> t-1), infinite
+    A_COUNT
+};
+
+enum Kind : int { K_SRC = 0, K_REAL = 1, K_SNK = 2 };
+
+struct Prob {
+    int Y, G, M, L;      // L = M-1 chain positions carry nodes
+    int P;               // Y*G
+    int pen, inh, hard;
+    int K;               // pulses per sweep
+    int bfs_cap;         // lateral relaxations per non-final global relabel (0 = exact)
+    int max_sweeps;      // honoured when capped
+    int capped;
+    int no_wave;         // skip the initial chain wave
+    const int32_t *lo, *hi;   // windowed only
+    int32_t *vol, *cu, *ph, *pv, *dar, *dbr, *dad, *dbd;
+    int32_t *e, *ein, *h, *h2;
+    int32_t *reach, *reach2, *labels;
+    unsigned long long *ctr;  // counters, see CTR_*
+};
+
+enum Ctr : int {
+    CTR_FLOW = 0, CTR_OFFSET, CTR_PRESAT, CTR_PUSHES, CTR_RELABELS, CTR_ENERGY, CTR_HARDVIOL,
+    CTR_SWEEPS, CTR_BFS_PASSES, CTR_REACH_PASSES, CTR_STATUS, CTR_CONVERGED, CTR_STRANDED, CTR_PULSES,
+    CTR_FLAG0 = 16,     // 3 rotating "changed" flags
+    CTR_ACT0 = 20,      // 3 rotating active counters
+    CTR_COUNT = 32
+};
+
+__host__ __device__ inline size_t plane_elems(int M, int P) { return (size_t)M * (size_t)P; }
+
+}  // namespace gz

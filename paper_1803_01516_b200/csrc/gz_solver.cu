@@ -1,0 +1,963 @@
+// gz_solver.cu -- B200 (sm_100a) push-relabel max-flow / min-cut on the
+// implicit gaze-line graph, plus the data term, energy and hierarchy helpers,
+// exported through the C ABI declared in include/gazecut_b200.h.
+//
+// Reference path (paths under /root/reference/pkg/src/gazecut/):
+//   sad_volume          energy.py:83-114      -> k_sad_planar / gz_sad_volume
+//   build_network       flownet.py:233-296    -> phase_init (implicit graph, no CSR)
+//   maxflow_push_relabel maxflow.py:403-478   -> gz_solve_kernel (persistent, cooperative)
+//   _global_relabel     maxflow.py:138-170    -> phase_bfs_* (exact BFS distance to the sink)
+//   _discharge_rounds   maxflow.py:183-250    -> phase_push / phase_relabel (synchronous pulses)
+//   _bfs_source_side    maxflow.py:267-284    -> phase_reach_* (prefix reach per chain)
+//   _extract_labels     maxflow.py:307-320    -> labels = lo + reach
+//   total_energy        energy.py:129-155     -> phase_energy (identity check, maxflow.py:501-505)
+//   coarsen / thin_skin hierarchy.py:39-73    -> k_coarsen / k_thin_skin
+//
+// The solver runs phase 1 of push-relabel only (no excess is returned to the
+// source).  The minimal source side of the minimum cut -- the set the
+// reference reads its labeling from -- is recovered exactly as the nodes
+// reachable in the residual graph from {source} U {nodes holding excess}; see
+// DESIGN.md section 3 for the argument and tests/test_gpu_parity.py for the
+// bit-exact checks against the oracle.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+
+#include "gazecut_b200.h"
+#include "gz_graph.cuh"
+
+namespace cg = cooperative_groups;
+using namespace gz;
+
+namespace {
+
+__device__ __forceinline__ int imin(int a, int b) { return a < b ? a : b; }
+
+// Per-column view: own window and the four neighbours (right, left, down, up).
+template <bool WIN>
+struct Col {
+    int c, y, g, lo, hi;
+    int nc[4], nlo[4], nhi[4];
+    bool has[4];
+
+    __device__ __forceinline__ void load(const Prob &p, int c_) {
+        c = c_;
+        y = c / p.G;
+        g = c - y * p.G;
+        has[0] = g + 1 < p.G; nc[0] = c + 1;
+        has[1] = g > 0;       nc[1] = c - 1;
+        has[2] = y + 1 < p.Y; nc[2] = c + p.G;
+        has[3] = y > 0;       nc[3] = c - p.G;
+        if (WIN) {
+            lo = p.lo[c]; hi = p.hi[c];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                nlo[i] = has[i] ? p.lo[nc[i]] : 0;
+                nhi[i] = has[i] ? p.hi[nc[i]] : 0;
+            }
+        } else {
+            lo = 0; hi = p.L;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) { nlo[i] = 0; nhi[i] = p.L; }
+        }
+    }
+    __device__ __forceinline__ int kind_own(int t) const { return t <= lo ? K_SRC : (t > hi ? K_SNK : K_REAL); }
+    __device__ __forceinline__ int kind_nb(int i, int t) const {
+        return t <= nlo[i] ? K_SRC : (t > nhi[i] ? K_SNK : K_REAL);
+    }
+};
+
+// Arc j out of real node (t, col): returns the residual (0 when the arc does
+// not exist), the target flat index (valid when kind == K_REAL), target kind.
+template <bool WIN>
+__device__ __forceinline__ int arc_resid(const Prob &p, const Col<WIN> &k, int j, int t, int &v, int &kind) {
+    const int P = p.P, c = k.c, L = p.L;
+    const int cap_i = p.hard ? HARD_CAP : p.inh;
+    kind = K_SRC;
+    v = 0;
+    switch (j) {
+    case A_UP:
+        kind = k.kind_own(t + 1); v = (t + 1) * P + c;
+        return p.cu[t * P + c];
+    case A_DN:
+        kind = k.kind_own(t - 1); v = (t - 1) * P + c;
+        return HINF;
+    case A_SR:
+        if (!k.has[0]) return 0;
+        kind = k.kind_nb(0, t); v = t * P + k.nc[0];
+        return p.ph[t * P + c];
+    case A_SL:
+        if (!k.has[1]) return 0;
+        kind = k.kind_nb(1, t); v = t * P + k.nc[1];
+        return 2 * p.pen - p.ph[t * P + k.nc[1]];
+    case A_SD:
+        if (!k.has[2]) return 0;
+        kind = k.kind_nb(2, t); v = t * P + k.nc[2];
+        return p.pv[t * P + c];
+    case A_SU:
+        if (!k.has[3]) return 0;
+        kind = k.kind_nb(3, t); v = t * P + k.nc[3];
+        return 2 * p.pen - p.pv[t * P + k.nc[3]];
+    case A_UR:
+        if (!k.has[0] || t >= L) return 0;
+        kind = k.kind_nb(0, t + 1); v = (t + 1) * P + k.nc[0];
+        return p.dbr[(t + 1) * P + c];
+    case A_UL:
+        if (!k.has[1] || t >= L) return 0;
+        kind = k.kind_nb(1, t + 1); v = (t + 1) * P + k.nc[1];
+        return p.dar[(t + 1) * P + k.nc[1]];
+    case A_UD:
+        if (!k.has[2] || t >= L) return 0;
+        kind = k.kind_nb(2, t + 1); v = (t + 1) * P + k.nc[2];
+        return p.dbd[(t + 1) * P + c];
+    case A_UU:
+        if (!k.has[3] || t >= L) return 0;
+        kind = k.kind_nb(3, t + 1); v = (t + 1) * P + k.nc[3];
+        return p.dad[(t + 1) * P + k.nc[3]];
+    case A_DR:
+        if (!k.has[0]) return 0;
+        kind = k.kind_nb(0, t - 1); v = (t - 1) * P + k.nc[0];
+        return cap_i - p.dar[t * P + c];
+    case A_DL:
+        if (!k.has[1]) return 0;
+        kind = k.kind_nb(1, t - 1); v = (t - 1) * P + k.nc[1];
+        return cap_i - p.dbr[t * P + k.nc[1]];
+    case A_DD:
+        if (!k.has[2]) return 0;
+        kind = k.kind_nb(2, t - 1); v = (t - 1) * P + k.nc[2];
+        return cap_i - p.dad[t * P + c];
+    case A_DU:
+        if (!k.has[3]) return 0;
+        kind = k.kind_nb(3, t - 1); v = (t - 1) * P + k.nc[3];
+        return cap_i - p.dbd[t * P + k.nc[3]];
+    }
+    return 0;
+}
+
+// Push d units along arc j out of (t, col): update the stored residual/flow.
+template <bool WIN>
+__device__ __forceinline__ void arc_push(const Prob &p, const Col<WIN> &k, int j, int t, int d) {
+    const int P = p.P, c = k.c;
+    switch (j) {
+    case A_UP: p.cu[t * P + c] -= d; break;
+    case A_DN: p.cu[(t - 1) * P + c] += d; break;
+    case A_SR: p.ph[t * P + c] -= d; break;
+    case A_SL: p.ph[t * P + k.nc[1]] += d; break;
+    case A_SD: p.pv[t * P + c] -= d; break;
+    case A_SU: p.pv[t * P + k.nc[3]] += d; break;
+    case A_UR: p.dbr[(t + 1) * P + c] -= d; break;
+    case A_UL: p.dar[(t + 1) * P + k.nc[1]] -= d; break;
+    case A_UD: p.dbd[(t + 1) * P + c] -= d; break;
+    case A_UU: p.dad[(t + 1) * P + k.nc[3]] -= d; break;
+    case A_DR: p.dar[t * P + c] += d; break;
+    case A_DL: p.dbr[t * P + k.nc[1]] += d; break;
+    case A_DD: p.dad[t * P + c] += d; break;
+    case A_DU: p.dbd[t * P + k.nc[3]] += d; break;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// initialisation: residuals from the volume, source saturation, chain wave,
+// constant offset (flownet.py:115-181 folded into an implicit graph;
+// maxflow.py:173-180 _saturate_source; maxflow.py:287-304 _chain_presaturate
+// generalised to a greedy upward wave along each chain).
+
+template <bool WIN>
+__device__ void phase_init_a(const Prob &p, int c) {
+    const int P = p.P;
+    for (int k = 0; k < p.M; ++k) {
+        p.cu[k * P + c] = p.vol[k * P + c];
+        p.ph[k * P + c] = p.pen;
+        p.pv[k * P + c] = p.pen;
+        p.dar[k * P + c] = 0; p.dbr[k * P + c] = 0; p.dad[k * P + c] = 0; p.dbd[k * P + c] = 0;
+        p.e[k * P + c] = 0; p.ein[k * P + c] = 0;
+    }
+}
+
+template <bool WIN>
+__device__ void phase_init_b(const Prob &p, int c, long long &flow, long long &offset, long long &presat) {
+    Col<WIN> k;
+    k.load(p, c);
+    const int P = p.P, L = p.L;
+    const long long icap_off = p.hard ? UNCUTTABLE : (long long)p.inh;
+    const int icap = p.hard ? HARD_CAP : p.inh;
+    if (WIN) {
+        // constant offset: source->sink arcs (flownet.py:124-125, 153-154, 172-173)
+        if (k.lo == k.hi) offset += p.vol[k.lo * P + c];
+        for (int i = 0; i < 4; i += 2) {   // forward neighbours: right (0), down (2)
+            if (!k.has[i]) continue;
+            for (int t = 1; t <= L; ++t) {
+                int a = k.kind_own(t), b = k.kind_nb(i, t);
+                if ((a == K_SRC && b == K_SNK) || (a == K_SNK && b == K_SRC)) offset += p.pen;
+                // diagonal dir 0: (c,t)->(n,t-1); dir 1: (n,t)->(c,t-1)
+                int a0 = k.kind_own(t), b0 = k.kind_nb(i, t - 1);
+                if (a0 == K_SRC && b0 == K_SNK) offset += icap_off;
+                int a1 = k.kind_nb(i, t), b1 = k.kind_own(t - 1);
+                if (a1 == K_SRC && b1 == K_SNK) offset += icap_off;
+            }
+        }
+        // saturate arcs leaving source positions into this column's real nodes
+        for (int t = k.lo + 1; t <= k.hi; ++t) {
+            long long add = 0;
+            if (t == k.lo + 1) add += p.vol[k.lo * P + c];           // chain arc lo
+            for (int i = 0; i < 4; ++i) {
+                if (!k.has[i]) continue;
+                if (k.kind_nb(i, t) == K_SRC) add += p.pen;           // same level
+                if (t + 1 <= L && k.kind_nb(i, t + 1) == K_SRC) add += icap;  // inhibit diagonal down into (c,t)
+            }
+            p.e[t * P + c] = (int)add;
+        }
+    } else {
+        p.e[1 * P + c] = p.vol[c];   // chain arc 0 from the source
+    }
+    // greedy wave up the chain: push as much as each chain arc admits
+    if (p.no_wave) return;
+    long long carry = 0;
+    for (int t = k.lo + 1; t <= k.hi; ++t) {
+        int x = p.e[t * P + c] + (int)carry;
+        int r = p.cu[t * P + c];
+        int d = imin(x, r);
+        p.cu[t * P + c] = r - d;
+        p.e[t * P + c] = x - d;
+        carry = d;
+    }
+    flow += carry;
+    presat += carry;
+}
+
+// ---------------------------------------------------------------------------
+// synchronous push pulse: every active node pushes on admissible arcs using the
+// height field as it stands (heights do not change during this phase, so no
+// two pushes on one arc pair can meet).  Own-column chain pushes feed the next
+// position immediately (Gauss-Seidel along the chain); lateral pushes land in
+// the neighbour's inbox `ein`, merged by the relabel phase.
+template <bool WIN>
+__device__ void phase_push(const Prob &p, int c, long long &flow, long long &pushes) {
+    Col<WIN> k;
+    k.load(p, c);
+    const int P = p.P;
+    for (int t = k.lo + 1; t <= k.hi; ++t) {
+        const int u = t * P + c;
+        int ex = p.e[u];
+        if (ex <= 0) continue;
+        const int hu = p.h[u];
+        if (hu >= HINF) continue;
+#pragma unroll
+        for (int j = 0; j < A_COUNT; ++j) {
+            if (ex <= 0) break;
+            int v, kind;
+            int r = arc_resid<WIN>(p, k, j, t, v, kind);
+            if (kind == K_SRC || r <= 0) continue;
+            int hv = kind == K_SNK ? 0 : p.h[v];
+            if (hu != hv + 1) continue;
+            int d = imin(ex, r);
+            arc_push<WIN>(p, k, j, t, d);
+            ex -= d;
+            ++pushes;
+            if (kind == K_SNK) flow += d;
+            else if (j == A_UP || j == A_DN) p.e[v] += d;
+            else atomicAdd(&p.ein[v], d);
+        }
+        p.e[u] = ex;
+    }
+}
+
+// relabel phase: merge the inbox, then every active node with no admissible
+// arc moves to one above its lowest residual neighbour (maxflow.py:217-228).
+// Reads h, writes h2 (snapshot semantics).
+template <bool WIN>
+__device__ void phase_relabel(const Prob &p, int c, long long &relabels) {
+    Col<WIN> k;
+    k.load(p, c);
+    const int P = p.P;
+    for (int t = k.lo + 1; t <= k.hi; ++t) {
+        const int u = t * P + c;
+        int ex = p.e[u] + p.ein[u];
+        p.ein[u] = 0;
+        p.e[u] = ex;
+        const int hu = p.h[u];
+        int hn = hu;
+        if (ex > 0 && hu < HINF) {
+            int best = HINF;
+            bool adm = false;
+#pragma unroll
+            for (int j = 0; j < A_COUNT; ++j) {
+                int v, kind;
+                int r = arc_resid<WIN>(p, k, j, t, v, kind);
+                if (kind == K_SRC || r <= 0) continue;
+                int hv = kind == K_SNK ? 0 : p.h[v];
+                if (hu == hv + 1) { adm = true; break; }
+                best = imin(best, hv + 1);
+            }
+            if (!adm) { hn = best; ++relabels; }
+        }
+        p.h2[u] = hn;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// global relabel: exact BFS distance to the sink over residual arcs
+// (maxflow.py:138-158).  Jacobi over lateral arcs (reads h, writes h2), then
+// the column is closed under its own chain arcs in registers-order sweeps.
+template <bool WIN>
+__device__ void phase_bfs_reset(const Prob &p, int c) {
+    for (int t = 1; t <= p.L; ++t) p.h[t * p.P + c] = HINF;
+}
+
+template <bool WIN>
+__device__ bool phase_bfs_iter(const Prob &p, int c) {
+    Col<WIN> k;
+    k.load(p, c);
+    const int P = p.P;
+    bool changed = false;
+    for (int t = k.lo + 1; t <= k.hi; ++t) {
+        const int u = t * P + c;
+        int best = p.h[u];
+#pragma unroll
+        for (int j = 0; j < A_DN; ++j) {    // all but chain-down (handled by the sweep)
+            int v, kind;
+            int r = arc_resid<WIN>(p, k, j, t, v, kind);
+            if (kind == K_SRC || r <= 0) continue;
+            int hv = kind == K_SNK ? 0 : p.h[v];
+            best = imin(best, hv + 1);
+        }
+        p.h2[u] = best;
+    }
+    // close the column under its chain arcs: down (t+1 -> t via cu[t] > 0) and
+    // up (t-1 reaches t's height + 1 through the infinite reverse arc)
+    for (int pass = 0; pass < 2; ++pass) {
+        int above = HINF;   // height of position t+1 (sink: 0)
+        for (int t = k.hi; t > k.lo; --t) {
+            const int u = t * P + c;
+            int hv = (t == k.hi) ? 0 : above;
+            int cur = p.h2[u];
+            if (p.cu[u] > 0 && hv + 1 < cur) { cur = hv + 1; p.h2[u] = cur; }
+            above = cur;
+        }
+        int below = HINF;
+        for (int t = k.lo + 1; t <= k.hi; ++t) {
+            const int u = t * P + c;
+            int cur = p.h2[u];
+            if (below < HINF && below + 1 < cur) { cur = below + 1; p.h2[u] = cur; }
+            below = cur;
+        }
+    }
+    for (int t = k.lo + 1; t <= k.hi; ++t) {
+        const int u = t * P + c;
+        if (p.h2[u] != p.h[u]) { changed = true; break; }
+    }
+    return changed;
+}
+
+// ---------------------------------------------------------------------------
+// extraction: the source side is downward closed along every chain (reverse
+// chain arcs are uncuttable), so it is one prefix length per site.  Seeds are
+// the nodes holding excess; closure over residual arcs to a fixpoint
+// (maxflow.py:267-284, 307-320).
+template <bool WIN>
+__device__ int column_close_up(const Prob &p, const Col<WIN> &k, int r) {
+    // reached real positions lo+1 .. lo+r; position q reaches q+1 if cu[q] > 0
+    const int P = p.P;
+    while (r > 0 && k.lo + r < k.hi && p.cu[(k.lo + r) * P + k.c] > 0) ++r;
+    return r;
+}
+
+template <bool WIN>
+__device__ void phase_reach_init(const Prob &p, int c) {
+    Col<WIN> k;
+    k.load(p, c);
+    int r = 0;
+    for (int t = k.hi; t > k.lo; --t)
+        if (p.e[t * p.P + c] > 0) { r = t - k.lo; break; }
+    p.reach[c] = column_close_up<WIN>(p, k, r);
+}
+
+// Highest position of column c reached from the reached prefix of neighbour i.
+template <bool WIN>
+__device__ __forceinline__ int reach_from_nb(const Prob &p, const Col<WIN> &k, int i, int rn, int best_pos) {
+    // neighbour i's reached real positions: nlo+1 .. nlo+rn.  Arcs from (n, q)
+    // into column c: same level (c,q), inhibit-down (c,q-1), reverse-diagonal up (c,q+1).
+    const int P = p.P, c = k.c, n = k.nc[i], L = p.L;
+    const int cap_i = p.hard ? HARD_CAP : p.inh;
+    const int top = k.nlo[i] + rn;
+    for (int q = top; q > k.nlo[i]; --q) {
+        if (q + 1 <= best_pos) break;   // nothing from here down can improve
+        // diagonal up: (n,q) -> (c,q+1) is the reverse of (c,q+1)->(n,q)
+        if (q + 1 <= L && q + 1 > best_pos && k.kind_own(q + 1) == K_REAL) {
+            int r = 0;
+            switch (i) {
+            case 0: r = p.dar[(q + 1) * P + c]; break;   // (c,q+1)->(c+1,q) flow = dar[q+1][c]
+            case 1: r = p.dbr[(q + 1) * P + n]; break;   // (c,q+1)->(c-1,q): pair (n,c) dir 1
+            case 2: r = p.dad[(q + 1) * P + c]; break;
+            case 3: r = p.dbd[(q + 1) * P + n]; break;
+            }
+            if (r > 0) best_pos = q + 1;
+        }
+        // same level: (n,q) -> (c,q)
+        if (q > best_pos && k.kind_own(q) == K_REAL) {
+            int r = 0;
+            switch (i) {
+            case 0: r = 2 * p.pen - p.ph[q * P + c]; break;   // (c+1,q)->(c,q)
+            case 1: r = p.ph[q * P + n]; break;               // (c-1,q)->(c,q)
+            case 2: r = 2 * p.pen - p.pv[q * P + c]; break;
+            case 3: r = p.pv[q * P + n]; break;
+            }
+            if (r > 0) best_pos = q;
+        }
+        // inhibit diagonal down: (n,q) -> (c,q-1)
+        if (q - 1 > best_pos && k.kind_own(q - 1) == K_REAL) {
+            int r = 0;
+            switch (i) {
+            case 0: r = cap_i - p.dbr[q * P + c]; break;   // (c+1,q)->(c,q-1): pair (c,c+1) dir 1
+            case 1: r = cap_i - p.dar[q * P + n]; break;   // (c-1,q)->(c,q-1): pair (n,c) dir 0
+            case 2: r = cap_i - p.dbd[q * P + c]; break;
+            case 3: r = cap_i - p.dad[q * P + n]; break;
+            }
+            if (r > 0) best_pos = q - 1;
+        }
+    }
+    return best_pos;
+}
+
+template <bool WIN>
+__device__ bool phase_reach_iter(const Prob &p, int c) {
+    Col<WIN> k;
+    k.load(p, c);
+    const int r0 = p.reach[c];
+    int best_pos = k.lo + r0;   // highest reached position (lo = none)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        if (!k.has[i]) continue;
+        int rn = p.reach[k.nc[i]];
+        if (rn > 0) best_pos = reach_from_nb<WIN>(p, k, i, rn, best_pos);
+    }
+    int r = column_close_up<WIN>(p, k, best_pos - k.lo);
+    p.reach2[c] = r;
+    return r != r0;
+}
+
+// energy.py:129-155 on the labeling (labels are cuboid-local)
+__device__ void phase_energy_col(const Prob &p, int c, long long &energy, int &viol) {
+    const int y = c / p.G, g = c - y * p.G;
+    const int a = p.labels[c];
+    energy += p.vol[a * p.P + c];
+    for (int i = 0; i < 2; ++i) {
+        bool has = i == 0 ? g + 1 < p.G : y + 1 < p.Y;
+        if (!has) continue;
+        int b = p.labels[i == 0 ? c + 1 : c + p.G];
+        int dl = a > b ? a - b : b - a;
+        if (p.hard && dl > 1) viol = 1;
+        energy += (long long)p.pen * dl + (long long)p.inh * (dl > 1 ? dl - 1 : 0);
+    }
+}
+
+__device__ __forceinline__ void warp_add_u64(unsigned long long *dst, long long v) {
+    unsigned long long x = (unsigned long long)v;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) == 0 && x) atomicAdd(dst, x);
+}
+
+// ---------------------------------------------------------------------------
+// The whole solve in one cooperative launch: no host round trips.
+template <bool WIN>
+__global__ void __launch_bounds__(256) gz_solve_kernel(Prob p) {
+    cg::grid_group grid = cg::this_grid();
+    const int stride = gridDim.x * blockDim.x;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int ncols_iter = (p.P + stride - 1) / stride;   // uniform trip count (warp-shuffle safety)
+    long long flow = 0, offset = 0, presat = 0, pushes = 0, relabels = 0;
+    volatile unsigned long long *vctr = p.ctr;
+
+    for (int it = 0, c = tid; it < ncols_iter; ++it, c += stride)
+        if (c < p.P) phase_init_a<WIN>(p, c);
+    grid.sync();
+    for (int it = 0, c = tid; it < ncols_iter; ++it, c += stride)
+        if (c < p.P) phase_init_b<WIN>(p, c, flow, offset, presat);
+    grid.sync();
+
+    int sweeps = 0, bfs_passes = 0, pulses = 0, flag_rot = 0, act_rot = 0;
+    int converged = 1;
+    const int bfs_guard = 4 * (p.P + p.M) + 64;
+    for (;;) {
+        // ---- global relabel (exact unless bfs_cap > 0) ----
+        for (int it = 0, c = tid; it < ncols_iter; ++it, c += stride)
+            if (c < p.P) phase_bfs_reset<WIN>(p, c);
+        grid.sync();
+        int iters = 0;
+        bool exact = true;
+        for (;;) {
+            bool ch = false;
+            for (int it = 0, c = tid; it < ncols_iter; ++it, c += stride)
+                if (c < p.P) ch |= phase_bfs_iter<WIN>(p, c);
+            if (tid == 0) vctr[CTR_FLAG0 + (flag_rot + 1) % 3] = 0;
+            if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) vctr[CTR_FLAG0 + flag_rot] = 1;
+            grid.sync();
+            bool any = vctr[CTR_FLAG0 + flag_rot] != 0;
+            flag_rot = (flag_rot + 1) % 3;
+            int32_t *tmp = p.h; p.h = p.h2; p.h2 = tmp;
+            ++iters;
+            if (!any) break;
+            if (p.bfs_cap > 0 && iters >= p.bfs_cap) { exact = false; break; }
+            if (iters > bfs_guard) { if (tid == 0) vctr[CTR_STATUS] = (unsigned long long)(-GZ_ERR_NOCONVERGE); break; }
+        }
+        bfs_passes += iters;
+        // ---- active nodes? ----
+        {
+            int cnt = 0;
+            for (int it = 0, c = tid; it < ncols_iter; ++it, c += stride) {
+                if (c >= p.P) continue;
+                int lo = WIN ? p.lo[c] : 0, hi = WIN ? p.hi[c] : p.L;
+                for (int t = lo + 1; t <= hi; ++t) {
+                    int u = t * p.P + c;
+                    cnt += (p.e[u] > 0 && p.h[u] < HINF);
+                }
+            }
+            if (tid == 0) vctr[CTR_ACT0 + (act_rot + 1) % 3] = 0;
+            warp_add_u64((unsigned long long *)&p.ctr[CTR_ACT0 + act_rot], cnt);
+            grid.sync();
+            unsigned long long act = vctr[CTR_ACT0 + act_rot];
+            act_rot = (act_rot + 1) % 3;
+            if (act == 0) {
+                if (exact) break;
+                // a truncated relabel found nothing: rerun it exactly before concluding
+                p.bfs_cap = 0;
+                continue;
+            }
+        }
+        if (p.capped && sweeps >= p.max_sweeps) { converged = 0; break; }
+        if (vctr[CTR_STATUS] != 0) break;
+        // ---- K synchronous push/relabel pulses ----
+        for (int pulse = 0; pulse < p.K; ++pulse) {
+            for (int it = 0, c = tid; it < ncols_iter; ++it, c += stride)
+                if (c < p.P) phase_push<WIN>(p, c, flow, pushes);
+            grid.sync();
+            for (int it = 0, c = tid; it < ncols_iter; ++it, c += stride)
+                if (c < p.P) phase_relabel<WIN>(p, c, relabels);
+            grid.sync();
+            int32_t *tmp = p.h; p.h = p.h2; p.h2 = tmp;
+            ++pulses;
+        }
+        ++sweeps;
+        if (sweeps > 1000000) { if (tid == 0) vctr[CTR_STATUS] = (unsigned long long)(-GZ_ERR_NOCONVERGE); break; }
+    }
+
+    // ---- extraction: reach closure from the excess nodes ----
+    for (int it = 0, c = tid; it < ncols_iter; ++it, c += stride)
+        if (c < p.P) phase_reach_init<WIN>(p, c);
+    grid.sync();
+    int reach_passes = 0;
+    const int reach_guard = 4 * (p.P + p.M) + 64;
+    for (;;) {
+        bool ch = false;
+        for (int it = 0, c = tid; it < ncols_iter; ++it, c += stride)
+            if (c < p.P) ch |= phase_reach_iter<WIN>(p, c);
+        if (tid == 0) vctr[CTR_FLAG0 + (flag_rot + 1) % 3] = 0;
+        if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) vctr[CTR_FLAG0 + flag_rot] = 1;
+        grid.sync();
+        bool any = vctr[CTR_FLAG0 + flag_rot] != 0;
+        flag_rot = (flag_rot + 1) % 3;
+        int32_t *tmp = p.reach; p.reach = p.reach2; p.reach2 = tmp;
+        ++reach_passes;
+        if (!any) break;
+        if (reach_passes > reach_guard) { if (tid == 0) vctr[CTR_STATUS] = (unsigned long long)(-GZ_ERR_NOCONVERGE); break; }
+    }
+    // labels, stranded excess
+    long long stranded = 0;
+    for (int it = 0, c = tid; it < ncols_iter; ++it, c += stride) {
+        if (c >= p.P) continue;
+        int lo = WIN ? p.lo[c] : 0, hi = WIN ? p.hi[c] : p.L;
+        p.labels[c] = lo + p.reach[c];
+        for (int t = lo + 1; t <= hi; ++t) stranded += p.e[t * p.P + c] > 0;
+    }
+    grid.sync();
+    long long energy = 0;
+    int viol = 0;
+    for (int it = 0, c = tid; it < ncols_iter; ++it, c += stride)
+        if (c < p.P) phase_energy_col(p, c, energy, viol);
+    warp_add_u64(&p.ctr[CTR_FLOW], flow);
+    warp_add_u64(&p.ctr[CTR_OFFSET], offset);
+    warp_add_u64(&p.ctr[CTR_PRESAT], presat);
+    warp_add_u64(&p.ctr[CTR_PUSHES], pushes);
+    warp_add_u64(&p.ctr[CTR_RELABELS], relabels);
+    warp_add_u64(&p.ctr[CTR_ENERGY], energy);
+    warp_add_u64(&p.ctr[CTR_STRANDED], stranded);
+    if (viol) p.ctr[CTR_HARDVIOL] = 1;
+    if (tid == 0) {
+        p.ctr[CTR_SWEEPS] = sweeps;
+        p.ctr[CTR_BFS_PASSES] = bfs_passes;
+        p.ctr[CTR_REACH_PASSES] = reach_passes;
+        p.ctr[CTR_CONVERGED] = converged;
+        p.ctr[CTR_PULSES] = pulses;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// data term (energy.py:83-114, geometry.py:325-335): one thread per site,
+// labels looped; output planar [k][y][g] (solver layout) or (y, g, k).
+template <bool PLANAR>
+__global__ void k_sad(const uint8_t *__restrict__ left, const uint8_t *__restrict__ right, int img_w, int ch,
+                      gz_cuboid cb, int32_t *__restrict__ vol) {
+    const int P = cb.y_extent * cb.g_extent;
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= P) return;
+    const int yi = c / cb.g_extent, gi = c - yi * cb.g_extent;
+    const int g = cb.g_min + gi;
+    const size_t row = (size_t)(cb.y_min + yi) * img_w * ch;
+    const uint8_t *lr = left + row, *rr = right + row;
+    for (int kk = 0; kk < cb.m; ++kk) {
+        const int d = cb.d_min + kk;
+        int xr = g + d, xl = (cb.width - 1) + g - d;
+        xr = xr < 0 ? 0 : (xr > cb.width - 1 ? cb.width - 1 : xr);
+        xl = xl < 0 ? 0 : (xl > cb.width - 1 ? cb.width - 1 : xl);
+        int acc = 0;
+        for (int q = 0; q < ch; ++q) acc += abs((int)lr[xl * ch + q] - (int)rr[xr * ch + q]);
+        if (PLANAR) vol[(size_t)kk * P + c] = acc;
+        else vol[(size_t)c * cb.m + kk] = acc;
+    }
+}
+
+// (rows, cols, m) -> planar [k][rows*cols]
+__global__ void k_to_planar(const int32_t *__restrict__ src, int P, int M, int32_t *__restrict__ dst) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= P) return;
+    for (int k = 0; k < M; ++k) dst[(size_t)k * P + c] = src[(size_t)c * M + k];
+}
+
+__global__ void k_total_energy(const int32_t *__restrict__ lab, const int32_t *__restrict__ vol, int rows, int cols,
+                               int m, gz_energy en, unsigned long long *out) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int P = rows * cols;
+    long long acc = 0;
+    int viol = 0;
+    if (c < P) {
+        const int y = c / cols, g = c - y * cols;
+        const int a = lab[c];
+        acc += vol[(size_t)c * m + a];
+        for (int i = 0; i < 2; ++i) {
+            bool has = i == 0 ? g + 1 < cols : y + 1 < rows;
+            if (!has) continue;
+            int b = lab[i == 0 ? c + 1 : c + cols];
+            int dl = a > b ? a - b : b - a;
+            if (en.hard_inhibit && dl > 1) viol = 1;
+            acc += (long long)en.penalty * dl + (long long)en.inhibit * (dl > 1 ? dl - 1 : 0);
+        }
+    }
+    warp_add_u64(&out[0], acc);
+    if (viol) out[1] = 1;
+}
+
+// hierarchy.py:39-57: coarse[Y][X][Z] = sum of the (zero padded) b^3 cube
+__global__ void k_coarsen(const int32_t *__restrict__ vol, int rows, int cols, int m, int b, int32_t *__restrict__ out) {
+    const int rb = (rows + b - 1) / b, cb = (cols + b - 1) / b, mb = (m + b - 1) / b;
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (long long)rb * cb * mb) return;
+    const int z = (int)(idx % mb);
+    const int x = (int)((idx / mb) % cb);
+    const int yb = (int)(idx / ((long long)mb * cb));
+    long long acc = 0;
+    for (int dy = 0; dy < b; ++dy) {
+        int y = yb * b + dy;
+        if (y >= rows) break;
+        for (int dx = 0; dx < b; ++dx) {
+            int g = x * b + dx;
+            if (g >= cols) break;
+            const int32_t *src = vol + ((size_t)y * cols + g) * m;
+            for (int dz = 0; dz < b; ++dz) {
+                int k = z * b + dz;
+                if (k >= m) break;
+                acc += src[k];
+            }
+        }
+    }
+    out[idx] = (int32_t)acc;
+}
+
+// hierarchy.py:60-73
+__global__ void k_thin_skin(const int32_t *__restrict__ coarse, int crows, int ccols, int rows, int cols, int m,
+                            int b, int radius, int32_t *__restrict__ lo, int32_t *__restrict__ hi) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= rows * cols) return;
+    const int y = c / cols, g = c - y * cols;
+    const int D = coarse[(y / b) * ccols + (g / b)];
+    long long l = (long long)b * (D - radius), h = (long long)b * (D + radius + 1) - 1;
+    lo[c] = (int32_t)(l < 0 ? 0 : l);
+    hi[c] = (int32_t)(h > m - 1 ? m - 1 : h);
+    (void)crows;
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+struct Workspace {
+    int32_t *vol, *cu, *ph, *pv, *dar, *dbr, *dad, *dbd, *e, *ein, *h, *h2;
+    int32_t *reach, *reach2, *labels;
+    unsigned long long *ctr;
+};
+
+size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+size_t ws_bytes(int rows, int cols, int m) {
+    const size_t P = (size_t)rows * cols, plane = align_up((size_t)m * P * 4), col = align_up(P * 4);
+    return 12 * plane + 3 * col + align_up(gz::CTR_COUNT * 8) + 256;
+}
+
+Workspace carve(void *ws, int rows, int cols, int m) {
+    const size_t P = (size_t)rows * cols, plane = align_up((size_t)m * P * 4), col = align_up(P * 4);
+    uint8_t *b = (uint8_t *)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+    Workspace w;
+    int32_t **planes[12] = {&w.vol, &w.cu, &w.ph, &w.pv, &w.dar, &w.dbr, &w.dad, &w.dbd, &w.e, &w.ein, &w.h, &w.h2};
+    for (int i = 0; i < 12; ++i) { *planes[i] = (int32_t *)b; b += plane; }
+    w.reach = (int32_t *)b; b += col;
+    w.reach2 = (int32_t *)b; b += col;
+    w.labels = (int32_t *)b; b += col;
+    w.ctr = (unsigned long long *)b;
+    return w;
+}
+
+#define CK(x)                                                                                  \
+    do {                                                                                       \
+        cudaError_t err__ = (x);                                                               \
+        if (err__ != cudaSuccess) {                                                            \
+            fprintf(stderr, "gazecut_b200: %s failed: %s\n", #x, cudaGetErrorString(err__));   \
+            return GZ_ERR_CUDA;                                                                \
+        }                                                                                      \
+    } while (0)
+
+int coop_grid(const void *kernel, int threads, int *grid_out) {
+    int dev = 0, sms = 0, occ = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, 0));
+    if (occ < 1) return GZ_ERR_CUDA;
+    *grid_out = sms * occ;
+    return GZ_OK;
+}
+
+// Solve one problem whose planar volume is already in w.vol.
+int solve_planar(const Workspace &w, int rows, int cols, int m, const gz_energy *en, const gz_sched *sc,
+                 const int32_t *lo, const int32_t *hi, int32_t *labels_out, gz_stats *st, cudaStream_t s) {
+    Prob p;
+    memset(&p, 0, sizeof(p));
+    p.Y = rows; p.G = cols; p.M = m; p.L = m - 1; p.P = rows * cols;
+    p.pen = en->penalty; p.inh = en->inhibit; p.hard = en->hard_inhibit ? 1 : 0;
+    p.K = sc && sc->rounds_per_sweep > 0 ? sc->rounds_per_sweep : 12;
+    p.bfs_cap = sc ? sc->bfs_cap : 0;
+    p.max_sweeps = sc ? sc->max_sweeps : 0;
+    p.no_wave = sc ? (sc->flags & GZ_SCHED_NO_WAVE) : 0;
+    p.capped = sc ? ((sc->flags & GZ_SCHED_CAPPED) != 0) : 0;
+    p.lo = lo; p.hi = hi;
+    p.vol = w.vol; p.cu = w.cu; p.ph = w.ph; p.pv = w.pv; p.dar = w.dar; p.dbr = w.dbr; p.dad = w.dad; p.dbd = w.dbd;
+    p.e = w.e; p.ein = w.ein; p.h = w.h; p.h2 = w.h2; p.reach = w.reach; p.reach2 = w.reach2; p.labels = w.labels;
+    p.ctr = w.ctr;
+    CK(cudaMemsetAsync(w.ctr, 0, gz::CTR_COUNT * 8, s));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, s));
+    const bool win = lo != nullptr;
+    const void *kern = win ? (const void *)gz_solve_kernel<true> : (const void *)gz_solve_kernel<false>;
+    int grid = 0;
+    int rc = coop_grid(kern, 256, &grid);
+    if (rc) return rc;
+    const int need = (p.P + 255) / 256;
+    if (grid > need) grid = need < 1 ? 1 : need;
+    void *args[] = {&p};
+    CK(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(256), args, 0, s));
+    CK(cudaEventRecord(e1, s));
+    unsigned long long h_ctr[gz::CTR_COUNT];
+    CK(cudaMemcpyAsync(h_ctr, w.ctr, sizeof(h_ctr), cudaMemcpyDeviceToHost, s));
+    if (labels_out && labels_out != w.labels)
+        CK(cudaMemcpyAsync(labels_out, w.labels, (size_t)p.P * 4, cudaMemcpyDeviceToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (h_ctr[CTR_STATUS]) return -(int)h_ctr[CTR_STATUS];
+    if (st) {
+        memset(st, 0, sizeof(*st));
+        st->flow = (int64_t)h_ctr[CTR_FLOW];
+        if (p.hard) {   // rescale uncuttable multiples to the reference's 2^56 (see gz_graph.cuh)
+            const int64_t k = st->flow / HARD_CAP, f = st->flow % HARD_CAP;
+            st->flow = k * (int64_t)gz::UNCUTTABLE + f;
+        }
+        st->const_offset = (int64_t)h_ctr[CTR_OFFSET];
+        st->presaturated = (int64_t)h_ctr[CTR_PRESAT];
+        st->pushes = (int64_t)h_ctr[CTR_PUSHES];
+        st->relabels = (int64_t)h_ctr[CTR_RELABELS];
+        st->labeling_energy = h_ctr[CTR_HARDVIOL] ? (int64_t)gz::UNCUTTABLE : (int64_t)h_ctr[CTR_ENERGY];
+        st->converged = (int32_t)h_ctr[CTR_CONVERGED];
+        st->energy = st->converged ? st->flow + st->const_offset : st->labeling_energy;
+        st->sweeps = (int32_t)h_ctr[CTR_SWEEPS];
+        st->stranded_excess_nodes = (int32_t)h_ctr[CTR_STRANDED];
+        st->bfs_passes = (int32_t)h_ctr[CTR_BFS_PASSES];
+        st->reach_passes = (int32_t)h_ctr[CTR_REACH_PASSES];
+        st->pulses = (int32_t)h_ctr[CTR_PULSES];
+        st->ms_total = ms;
+    }
+    return GZ_OK;
+}
+
+int check_sm100() {
+    int dev = 0, major = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+    return major == 10 ? GZ_OK : GZ_ERR_NOGPU;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+extern "C" {
+
+size_t gz_workspace_bytes(int32_t rows, int32_t cols, int32_t m) {
+    if (rows < 1 || cols < 1 || m < 1) return 0;
+    return ws_bytes(rows, cols, m);
+}
+
+int gz_sad_volume(const uint8_t *left, const uint8_t *right, int32_t img_h, int32_t img_w, int32_t channels,
+                  const gz_cuboid *cb, int32_t *vol_out, void *stream) {
+    if (!cb || !left || !right || !vol_out || channels < 1) return GZ_ERR_ARG;
+    if (cb->y_min < 0 || cb->y_min + cb->y_extent > img_h || cb->g_extent < 1 || cb->m < 1) return GZ_ERR_ARG;
+    const int P = cb->y_extent * cb->g_extent;
+    k_sad<false><<<(P + 127) / 128, 128, 0, (cudaStream_t)stream>>>(left, right, img_w, channels, *cb, vol_out);
+    CK(cudaGetLastError());
+    return GZ_OK;
+}
+
+int gz_solve_volume(const int32_t *vol, int32_t rows, int32_t cols, int32_t m, const gz_energy *energy,
+                    const gz_sched *sched, const int32_t *lo, const int32_t *hi, int32_t *labels_out,
+                    gz_stats *stats_out, void *workspace, size_t workspace_bytes, void *stream) {
+    if (!vol || !energy || rows < 1 || cols < 1 || m < 1 || (!lo) != (!hi)) return GZ_ERR_ARG;
+    if (energy->penalty < 0 || energy->inhibit < 0) return GZ_ERR_ARG;
+    if (workspace_bytes < ws_bytes(rows, cols, m)) return GZ_ERR_WORKSPACE;
+    int rc = check_sm100();
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    Workspace w = carve(workspace, rows, cols, m);
+    const int P = rows * cols;
+    k_to_planar<<<(P + 255) / 256, 256, 0, s>>>(vol, P, m, w.vol);
+    CK(cudaGetLastError());
+    if (m == 1) {
+        // single label: everything folds into the offset (flownet.py:305-322)
+        CK(cudaMemsetAsync(labels_out ? labels_out : w.labels, 0, (size_t)P * 4, s));
+        unsigned long long *d = w.ctr;
+        CK(cudaMemsetAsync(d, 0, 16, s));
+        gz_energy en = *energy;
+        k_total_energy<<<(P + 255) / 256, 256, 0, s>>>(labels_out ? labels_out : w.labels, vol, rows, cols, 1, en, d);
+        unsigned long long hv[2];
+        CK(cudaMemcpyAsync(hv, d, 16, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (stats_out) {
+            memset(stats_out, 0, sizeof(*stats_out));
+            stats_out->const_offset = (int64_t)hv[0];
+            stats_out->energy = stats_out->labeling_energy = (int64_t)hv[0];
+            stats_out->converged = 1;
+        }
+        return GZ_OK;
+    }
+    return solve_planar(w, rows, cols, m, energy, sched, lo, hi, labels_out, stats_out, s);
+}
+
+int gz_solve_pairs(const uint8_t *left, const uint8_t *right, int32_t batch, int32_t img_h, int32_t img_w,
+                   int32_t channels, const gz_cuboid *cb, const gz_energy *energy, const gz_sched *sched,
+                   int32_t *labels_out, gz_stats *stats_out, void *workspace, size_t workspace_bytes,
+                   void *stream) {
+    if (!cb || !energy || batch < 1 || channels < 1 || cb->m < 2) return GZ_ERR_ARG;
+    if (cb->y_min < 0 || cb->y_min + cb->y_extent > img_h) return GZ_ERR_ARG;
+    const int rows = cb->y_extent, cols = cb->g_extent, m = cb->m, P = rows * cols;
+    const size_t one = ws_bytes(rows, cols, m);
+    if (workspace_bytes < one) return GZ_ERR_WORKSPACE;
+    int rc = check_sm100();
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    Workspace w = carve(workspace, rows, cols, m);
+    const size_t img = (size_t)img_h * img_w * channels;
+    for (int b = 0; b < batch; ++b) {
+        k_sad<true><<<(P + 127) / 128, 128, 0, s>>>(left + b * img, right + b * img, img_w, channels, *cb, w.vol);
+        CK(cudaGetLastError());
+        rc = solve_planar(w, rows, cols, m, energy, sched, nullptr, nullptr, labels_out + (size_t)b * P,
+                          stats_out ? stats_out + b : nullptr, s);
+        if (rc) return rc;
+        if (stats_out && stats_out[b].energy != stats_out[b].labeling_energy) return GZ_ERR_CONSISTENCY;
+    }
+    return GZ_OK;
+}
+
+int gz_solve_pairs_host(const uint8_t *left_host, const uint8_t *right_host, int32_t batch, int32_t img_h,
+                        int32_t img_w, int32_t channels, const gz_cuboid *cb, const gz_energy *energy,
+                        const gz_sched *sched, int32_t *labels_host, gz_stats *stats_host, void *workspace,
+                        size_t workspace_bytes, void *stream) {
+    if (!cb || batch < 1) return GZ_ERR_ARG;
+    const int P = cb->y_extent * cb->g_extent;
+    const size_t img = (size_t)img_h * img_w * channels * batch;
+    const size_t one = ws_bytes(cb->y_extent, cb->g_extent, cb->m);
+    const size_t need = one + 2 * align_up(img) + align_up((size_t)batch * P * 4);
+    if (workspace_bytes < need) return GZ_ERR_WORKSPACE;
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t *base = (uint8_t *)(((uintptr_t)workspace + 255) & ~(uintptr_t)255);
+    uint8_t *dl = base + one, *dr = dl + align_up(img);
+    int32_t *dlab = (int32_t *)(dr + align_up(img));
+    CK(cudaMemcpyAsync(dl, left_host, img, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(dr, right_host, img, cudaMemcpyHostToDevice, s));
+    int rc = gz_solve_pairs(dl, dr, batch, img_h, img_w, channels, cb, energy, sched, dlab, stats_host, base, one, s);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(labels_host, dlab, (size_t)batch * P * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return GZ_OK;
+}
+
+int gz_total_energy(const int32_t *labels, const int32_t *vol, int32_t rows, int32_t cols, int32_t m,
+                    const gz_energy *energy, int64_t *energy_out, void *stream) {
+    if (!labels || !vol || !energy || !energy_out || rows < 1 || cols < 1 || m < 1) return GZ_ERR_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    // energy_out must hold 2 int64: [0] energy, [1] hard-inhibit violation flag
+    CK(cudaMemsetAsync(energy_out, 0, 16, s));
+    const int P = rows * cols;
+    k_total_energy<<<(P + 255) / 256, 256, 0, s>>>(labels, vol, rows, cols, m, *energy,
+                                                   (unsigned long long *)energy_out);
+    CK(cudaGetLastError());
+    return GZ_OK;
+}
+
+int gz_coarsen(const int32_t *vol, int32_t rows, int32_t cols, int32_t m, int32_t block, int32_t *coarse_out,
+               void *stream) {
+    if (!vol || !coarse_out || block < 1 || rows < 1 || cols < 1 || m < 1) return GZ_ERR_ARG;
+    const long long n = (long long)((rows + block - 1) / block) * ((cols + block - 1) / block) * ((m + block - 1) / block);
+    k_coarsen<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(vol, rows, cols, m, block, coarse_out);
+    CK(cudaGetLastError());
+    return GZ_OK;
+}
+
+int gz_thin_skin(const int32_t *coarse_labels, int32_t crows, int32_t ccols, int32_t rows, int32_t cols, int32_t m,
+                 int32_t block, int32_t radius, int32_t *lo_out, int32_t *hi_out, void *stream) {
+    if (!coarse_labels || !lo_out || !hi_out || block < 1 || radius < 0) return GZ_ERR_ARG;
+    const int P = rows * cols;
+    k_thin_skin<<<(P + 255) / 256, 256, 0, (cudaStream_t)stream>>>(coarse_labels, crows, ccols, rows, cols, m, block,
+                                                                  radius, lo_out, hi_out);
+    CK(cudaGetLastError());
+    return GZ_OK;
+}
+
+const char *gz_status_string(int status) {
+    switch (status) {
+    case GZ_OK: return "ok";
+    case GZ_ERR_ARG: return "invalid argument";
+    case GZ_ERR_CUDA: return "CUDA runtime error";
+    case GZ_ERR_WORKSPACE: return "workspace too small";
+    case GZ_ERR_CONSISTENCY: return "cut cost != labeling energy";
+    case GZ_ERR_OVERFLOW: return "capacities exceed the int32 device state";
+    case GZ_ERR_NOCONVERGE: return "iteration guard tripped";
+    case GZ_ERR_NOGPU: return "no sm_100 GPU";
+    }
+    return "unknown status";
+}
+
+const char *gz_build_info(void) { return "gazecut_b200 v1 sm_100a persistent-cooperative push-relabel"; }
+
+}  // extern "C"
