@@ -1,0 +1,89 @@
+"""GPU results against fixtures recorded from the reference (tests/golden/)."""
+
+import hashlib
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+GOLDEN = Path(__file__).resolve().parent / "golden"
+G = json.loads((GOLDEN / "golden.json").read_text())
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def test_random_cases(gz):
+    arr = np.load(GOLDEN / "random_cases.npz")
+    for i, meta in enumerate(G["random_cases"]):
+        p = gz.EnergyParams(meta["penalty"], meta["inhibit"], meta["hard"])
+        lo = arr[f"lo{i}"] if meta["windowed"] else None
+        hi = arr[f"hi{i}"] if meta["windowed"] else None
+        net = gz.build_network(arr[f"vol{i}"], p, lo, hi)
+        assert (net.n_nodes, net.num_arcs, net.const_offset) == (meta["nodes"], meta["arcs"], meta["const_offset"])
+        r = gz.maxflow_push_relabel(net)
+        assert r.flow == meta["flow"] and r.energy == meta["energy"], i
+        assert np.array_equal(r.labeling, arr[f"lab{i}"]), i
+        assert np.array_equal(r.source_side, arr[f"side{i}"]), i
+        assert gz.total_energy(r.labeling, arr[f"vol{i}"], p) == meta["total_energy"]
+
+
+def test_c1_seeds_exact_via_pairs(gz):
+    """BASELINE config 1 / 4: fused data term + exact cut, seeds 0..7."""
+    cub = gz.cuboid_from_disparity_range(384, 288, 10, 28, num_labels=16)
+    scenes = [gz.make_scene(s) for s in range(8)]
+    left = torch.from_numpy(np.stack([s.left for s in scenes]))
+    right = torch.from_numpy(np.stack([s.right for s in scenes]))
+    solver = gz.PairSolver(cub, gz.EnergyParams(14, 1023), 288, 384, 3)
+    labels, stats = solver.solve(left, right)
+    for seed, want in enumerate(G["c1_exact"]):
+        assert stats[seed]["flow"] == want["flow"] and stats[seed]["energy"] == want["energy"]
+        assert sha(labels[seed].cpu().numpy()) == want["labeling"], seed
+    # the same through the host-buffer (end-to-end) entry point
+    lab_h, st_h = solver.solve_host(left.numpy()[:2], right.numpy()[:2])
+    for seed in range(2):
+        assert sha(lab_h[seed]) == G["c1_exact"][seed]["labeling"]
+
+
+def test_c1_volume_matches_reference(gz):
+    cub = gz.cuboid_from_disparity_range(384, 288, 10, 28, num_labels=16)
+    sc = gz.make_scene(0)
+    assert sha(gz.sad_volume(sc.left, sc.right, cub)) == G["c1_exact"][0]["volume"]
+
+
+def test_ladder24(gz):
+    cub = gz.cuboid_from_disparity_range(384, 288, 10, 28, num_labels=24)
+    sc = gz.make_scene(0)
+    vol = gz.sad_volume(sc.left, sc.right, cub)
+    lad = G["ladder24"]
+    assert sha(vol) == lad["volume"]
+    p = gz.EnergyParams(14, 1023)
+    ex = gz.solve_exact(vol, p)
+    assert ex.energy == lad["exact"]["energy"] == 778554
+    assert sha(ex.labeling) == lad["exact"]["labeling"]
+    assert ex.stats["nodes"] == 2_464_130 and ex.stats["arcs"] == 33_766_536
+    for b, key in ((2, "l1b2"), (3, "l1b3")):
+        r = gz.solve_level1(vol, p, b)
+        assert r.energy == lad[key]["energy"] and sha(r.labeling) == lad[key]["labeling"], key
+        assert r.stats["coarse_energy"] == lad[key]["coarse_energy"]
+    l2 = gz.solve_level2(vol, p, 3)
+    assert lad["exact"]["energy"] <= lad["l1b3"]["energy"] <= l2.energy
+    l2u = gz.solve_level2(vol, p, 3, max_sweeps=None)
+    assert l2u.energy == lad["l1b3"]["energy"] and sha(l2u.labeling) == lad["l1b3"]["labeling"]
+
+
+def test_hierarchy_cases(gz):
+    arr = np.load(GOLDEN / "hierarchy_cases.npz")
+    for i, meta in enumerate(G["hierarchy_cases"]):
+        vol = arr[f"vol{i}"]
+        p = gz.EnergyParams(meta["penalty"], meta["inhibit"])
+        c, cp = gz.coarsen(vol, meta["block"], p)
+        assert np.array_equal(c, arr[f"coarse{i}"]) and cp.penalty == meta["coarse_penalty"]
+        l1 = gz.solve_level1(vol, p, meta["block"])
+        assert l1.energy == meta["l1_energy"] and np.array_equal(l1.labeling, arr[f"l1lab{i}"])
+        l2u = gz.solve_level2(vol, p, meta["block"], max_sweeps=None)
+        assert l2u.energy == meta["l2u_energy"]
