@@ -58,13 +58,16 @@ typedef struct {
 typedef struct {
     int32_t rounds_per_sweep;  /* synchronous push/relabel pulses per sweep (default 12) */
     int32_t max_sweeps;        /* sweep cap, honoured only with GZ_SCHED_CAPPED (level-2 mode) */
-    int32_t bfs_cap;           /* lateral BFS relaxations per non-final global relabel (0 = exact) */
+    int32_t bfs_cap;           /* BFS depth before a global relabel may stop at the first active node
+                                  (0 = library default, < 0 = exhaustive every sweep) */
     int32_t flags;             /* GZ_SCHED_NO_WAVE: skip the chain wave (maxflow.py:422 presaturate=False);
                                   GZ_SCHED_CAPPED: stop after max_sweeps sweeps (maxflow.py:447-449) */
 } gz_sched;
 
 #define GZ_SCHED_NO_WAVE 1
 #define GZ_SCHED_CAPPED 2
+#define GZ_SCHED_V1 4      /* force the v1 (column-relaxation) solver; debugging/comparison */
+#define GZ_SCHED_V2 8      /* force the v2 (bit-parallel, thread-per-chain) solver */
 
 /* maxflow.py:460-471 + 506-509 stats keys, plus device timings. */
 typedef struct {
@@ -72,7 +75,8 @@ typedef struct {
     int64_t labeling_energy;       /* energy.py:129-155 recomputed on device */
     int32_t sweeps, converged, stranded_excess_nodes, bfs_passes, reach_passes, pulses;
     float ms_total;                /* device time of the solve (CUDA events) */
-    float ms_reserved[3];
+    float ms_phase[6];             /* in-kernel phase times: init, mask build, global relabel, pulses,
+                                      extraction, energy/labels (v2 solver; 0 for v1) */
 } gz_stats;
 
 /* Device bytes the caller must provide as workspace for one problem of the

@@ -23,6 +23,8 @@ GZ_ERR_NOCONVERGE = -6
 GZ_ERR_NOGPU = -7
 GZ_SCHED_NO_WAVE = 1
 GZ_SCHED_CAPPED = 2
+GZ_SCHED_V1 = 4
+GZ_SCHED_V2 = 8
 
 
 class Cuboid(C.Structure):
@@ -46,7 +48,7 @@ class Stats(C.Structure):
                [(n, C.c_int32) for n in
                 ("sweeps", "converged", "stranded_excess_nodes", "bfs_passes", "reach_passes",
                  "pulses")] + \
-               [("ms_total", C.c_float), ("ms_reserved", C.c_float * 3)]
+               [("ms_total", C.c_float), ("ms_phase", C.c_float * 6)]
 
 
 class GazecutError(RuntimeError):

@@ -29,10 +29,13 @@
 namespace gz {
 
 constexpr int32_t HINF = 0x3fffffff;        // "cannot reach the sink"
-// Finite stand-in for UNCUTTABLE inhibit diagonals in hard mode.  A flow that
-// crosses k uncuttable arcs is k*HARD_CAP + f on the device and is reported as
-// k*2^56 + f, the reference's value (exact while f < HARD_CAP).
-constexpr int32_t HARD_CAP = 1 << 27;
+// Hard inhibit: UNCUTTABLE diagonals get a finite stand-in capacity p.hcap, a
+// power of two above the total finite source capacity of the problem (chosen
+// on the host by a device pre-pass).  A minimum cut that crosses k uncuttable
+// arcs then has value k*hcap + f with f < hcap on the device and is reported
+// as k*2^56 + f, the reference's value.  If (k_max+1)*hcap would not fit the
+// int32 state the solve returns GZ_ERR_OVERFLOW instead of a wrong answer.
+constexpr int32_t HARD_CAP_DEFAULT = 1 << 27;
 constexpr long long UNCUTTABLE = 1LL << 56; // energy.py:34
 
 // arc slots of a node, in push order
@@ -51,10 +54,13 @@ struct Prob {
     int Y, G, M, L;      // L = M-1 chain positions carry nodes
     int P;               // Y*G
     int pen, inh, hard;
+    int hcap;            // stand-in capacity of uncuttable inhibit arcs (hard mode)
     int K;               // pulses per sweep
     int bfs_cap;         // lateral relaxations per non-final global relabel (0 = exact)
     int max_sweeps;      // honoured when capped
     int capped;
+    unsigned long long watchdog_ns, t_start_ns;   // 0 = no watchdog; start stamped on device
+    volatile unsigned *progress;                  // debug: per-block phase counter (mapped host memory) or null
     int no_wave;         // skip the initial chain wave
     const int32_t *lo, *hi;   // windowed only
     int32_t *vol, *cu, *ph, *pv, *dar, *dbr, *dad, *dbd;
@@ -68,6 +74,7 @@ enum Ctr : int {
     CTR_SWEEPS, CTR_BFS_PASSES, CTR_REACH_PASSES, CTR_STATUS, CTR_CONVERGED, CTR_STRANDED, CTR_PULSES,
     CTR_FLAG0 = 16,     // 3 rotating "changed" flags
     CTR_ACT0 = 20,      // 3 rotating active counters
+    CTR_T0 = 24,        // 6 phase timers (ns): init, mask build, bfs, pulses, reach, tail
     CTR_COUNT = 32
 };
 

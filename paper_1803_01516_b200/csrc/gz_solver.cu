@@ -24,7 +24,10 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <ctime>
+#include <unistd.h>
 
 #include "gazecut_b200.h"
 #include "gz_graph.cuh"
@@ -75,7 +78,7 @@ struct Col {
 template <bool WIN>
 __device__ __forceinline__ int arc_resid(const Prob &p, const Col<WIN> &k, int j, int t, int &v, int &kind) {
     const int P = p.P, c = k.c, L = p.L;
-    const int cap_i = p.hard ? HARD_CAP : p.inh;
+    const int cap_i = p.hard ? p.hcap : p.inh;
     kind = K_SRC;
     v = 0;
     switch (j) {
@@ -183,7 +186,7 @@ __device__ void phase_init_b(const Prob &p, int c, long long &flow, long long &o
     k.load(p, c);
     const int P = p.P, L = p.L;
     const long long icap_off = p.hard ? UNCUTTABLE : (long long)p.inh;
-    const int icap = p.hard ? HARD_CAP : p.inh;
+    const int icap = p.hard ? p.hcap : p.inh;
     if (WIN) {
         // constant offset: source->sink arcs (flownet.py:124-125, 153-154, 172-173)
         if (k.lo == k.hi) offset += p.vol[k.lo * P + c];
@@ -381,7 +384,7 @@ __device__ __forceinline__ int reach_from_nb(const Prob &p, const Col<WIN> &k, i
     // neighbour i's reached real positions: nlo+1 .. nlo+rn.  Arcs from (n, q)
     // into column c: same level (c,q), inhibit-down (c,q-1), reverse-diagonal up (c,q+1).
     const int P = p.P, c = k.c, n = k.nc[i], L = p.L;
-    const int cap_i = p.hard ? HARD_CAP : p.inh;
+    const int cap_i = p.hard ? p.hcap : p.inh;
     const int top = k.nlo[i] + rn;
     for (int q = top; q > k.nlo[i]; --q) {
         if (q + 1 <= best_pos) break;   // nothing from here down can improve
@@ -595,10 +598,18 @@ __global__ void __launch_bounds__(256) gz_solve_kernel(Prob p) {
     }
 }
 
+}  // namespace
+
+#include "gz_bitsolve.cuh"
+#include "gz_warpsolve.cuh"
+
+namespace {
+
 // ---------------------------------------------------------------------------
 // data term (energy.py:83-114, geometry.py:325-335): one thread per site,
 // labels looped; output planar [k][y][g] (solver layout) or (y, g, k).
-template <bool PLANAR>
+// LAYOUT 0: (y, g, k) reference order; 1: planar [k][site]; 2: column-major [site][LP]
+template <int LAYOUT, int LP = 16>
 __global__ void k_sad(const uint8_t *__restrict__ left, const uint8_t *__restrict__ right, int img_w, int ch,
                       gz_cuboid cb, int32_t *__restrict__ vol) {
     const int P = cb.y_extent * cb.g_extent;
@@ -615,9 +626,51 @@ __global__ void k_sad(const uint8_t *__restrict__ left, const uint8_t *__restric
         xl = xl < 0 ? 0 : (xl > cb.width - 1 ? cb.width - 1 : xl);
         int acc = 0;
         for (int q = 0; q < ch; ++q) acc += abs((int)lr[xl * ch + q] - (int)rr[xr * ch + q]);
-        if (PLANAR) vol[(size_t)kk * P + c] = acc;
+        if (LAYOUT == 1) vol[(size_t)kk * P + c] = acc;
+        else if (LAYOUT == 2) vol[(size_t)c * LP + kk] = acc;
         else vol[(size_t)c * cb.m + kk] = acc;
     }
+    if (LAYOUT == 2)
+        for (int kk = cb.m; kk < LP; ++kk) vol[(size_t)c * LP + kk] = 0;
+}
+
+// (rows, cols, m) -> column-major [site][LP], zero padded
+template <int LP>
+__global__ void k_to_colmajor(const int32_t *__restrict__ src, int P, int M, int32_t *__restrict__ dst) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long long)P * LP) return;
+    const int c = (int)(i / LP), k = (int)(i % LP);
+    dst[i] = k < M ? src[(size_t)c * M + k] : 0;
+}
+
+// Source-capacity census (windows or hard mode): out[0] += finite capacity of
+// arcs leaving source positions into real nodes, out[1] += number of such
+// arcs that are uncuttable (hard inhibit diagonals).  vol: (rows, cols, m).
+__global__ void k_source_caps(const int32_t *__restrict__ vol, int rows, int cols, int m, const int32_t *lo,
+                              const int32_t *hi, gz_energy en, unsigned long long *out) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int P = rows * cols;
+    unsigned long long fin = 0, inf = 0;
+    if (c < P) {
+        const int y = c / cols, g = c - y * cols;
+        const int l0 = lo ? lo[c] : 0, h0 = hi ? hi[c] : m - 1;
+        if (h0 > l0) fin += (unsigned long long)vol[(size_t)c * m + l0];   // chain arc lo
+        const int nc[4] = {c + 1, c - 1, c + cols, c - cols};
+        const bool has[4] = {g + 1 < cols, g > 0, y + 1 < rows, y > 0};
+        for (int i = 0; i < 4; ++i) {
+            if (!has[i]) continue;
+            const int ln = lo ? lo[nc[i]] : 0;
+            for (int t = l0 + 1; t <= h0; ++t) {
+                if (t <= ln) fin += (unsigned long long)en.penalty;                // same level from a source position
+                if (t + 1 <= m - 1 && t + 1 <= ln) {                                // inhibit diagonal (n,t+1)->(c,t)
+                    if (en.hard_inhibit) ++inf;
+                    else fin += (unsigned long long)en.inhibit;
+                }
+            }
+        }
+    }
+    warp_add_u64(&out[0], (long long)fin);
+    warp_add_u64(&out[1], (long long)inf);
 }
 
 // (rows, cols, m) -> planar [k][rows*cols]
@@ -696,17 +749,38 @@ struct Workspace {
     int32_t *vol, *cu, *ph, *pv, *dar, *dbr, *dad, *dbd, *e, *ein, *h, *h2;
     int32_t *reach, *reach2, *labels;
     unsigned long long *ctr;
+    gz2::Bits2 bits;
+    uint32_t *IN0, *IN1;
+    uint32_t *bits_base;
+    size_t bits_bytes;
 };
 
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// words per column of the bit-parallel solver (positions 1..m), rounded to a template instance
+int words_for(int m) {
+    const int w = (m + 31) / 32;
+    return w <= 1 ? 1 : w <= 2 ? 2 : w <= 4 ? 4 : w <= 8 ? 8 : 0;
+}
+
+size_t bit_bytes(int rows, int cols, int m) {
+    const size_t P = (size_t)rows * cols;
+    const int NW = words_for(m) ? words_for(m) : 1;
+    return align_up((size_t)(13 + 9) * NW * P * 4) + 2 * align_up(P * 4);
+}
+
+// lanes per chain segment of the v3 solver (0: m too large for it)
+int lanes_for(int m) { return m <= 16 ? 16 : (m <= 32 ? 32 : 0); }
+
 size_t ws_bytes(int rows, int cols, int m) {
-    const size_t P = (size_t)rows * cols, plane = align_up((size_t)m * P * 4), col = align_up(P * 4);
-    return 12 * plane + 3 * col + align_up(gz::CTR_COUNT * 8) + 256;
+    const int mp = m > lanes_for(m) ? m : lanes_for(m);
+    const size_t P = (size_t)rows * cols, plane = align_up((size_t)mp * P * 4), col = align_up(P * 4);
+    return 12 * plane + 3 * col + align_up(gz::CTR_COUNT * 8) + bit_bytes(rows, cols, m) + 256;
 }
 
 Workspace carve(void *ws, int rows, int cols, int m) {
-    const size_t P = (size_t)rows * cols, plane = align_up((size_t)m * P * 4), col = align_up(P * 4);
+    const int mp = m > lanes_for(m) ? m : lanes_for(m);
+    const size_t P = (size_t)rows * cols, plane = align_up((size_t)mp * P * 4), col = align_up(P * 4);
     uint8_t *b = (uint8_t *)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
     Workspace w;
     int32_t **planes[12] = {&w.vol, &w.cu, &w.ph, &w.pv, &w.dar, &w.dbr, &w.dad, &w.dbd, &w.e, &w.ein, &w.h, &w.h2};
@@ -714,7 +788,20 @@ Workspace carve(void *ws, int rows, int cols, int m) {
     w.reach = (int32_t *)b; b += col;
     w.reach2 = (int32_t *)b; b += col;
     w.labels = (int32_t *)b; b += col;
-    w.ctr = (unsigned long long *)b;
+    w.ctr = (unsigned long long *)b; b += align_up(gz::CTR_COUNT * 8);
+    const int NW = words_for(m) ? words_for(m) : 1;
+    w.bits_base = (uint32_t *)b;
+    w.bits_bytes = bit_bytes(rows, cols, m);
+    uint32_t *u = (uint32_t *)b;
+    const size_t word_plane = (size_t)NW * P;
+    w.bits.NW = NW;
+    w.bits.mask = u; u += 13 * word_plane;
+    uint32_t **arr[9] = {&w.bits.V, &w.bits.F0, &w.bits.F1, &w.bits.A, &w.bits.IN, &w.bits.EX, &w.bits.RL,
+                         &w.IN0, &w.IN1};
+    for (int i = 0; i < 9; ++i) { *arr[i] = u; u += word_plane; }
+    uint8_t *rb = (uint8_t *)(((uintptr_t)u + 255) & ~(uintptr_t)255);
+    w.bits.R0 = (int32_t *)rb; rb += col;
+    w.bits.R1 = (int32_t *)rb;
     return w;
 }
 
@@ -737,18 +824,33 @@ int coop_grid(const void *kernel, int threads, int *grid_out) {
     return GZ_OK;
 }
 
-// Solve one problem whose planar volume is already in w.vol.
+// 1: v1 column relaxation, 2: bit-parallel (any m <= 256, deterministic
+// relabel when capped), 3: warp-per-chain (m <= 32, exact / uncapped)
+int choose_solver(int m, const gz_sched *sc) {
+    const int flags = sc ? sc->flags : 0;
+    if ((flags & GZ_SCHED_V1) || words_for(m) == 0) return 1;
+    if ((flags & GZ_SCHED_V2) || (flags & GZ_SCHED_CAPPED) || lanes_for(m) == 0) return 2;
+    return 3;
+}
+
+// Solve one problem whose volume is already in w.vol (layout of the chosen solver).
 int solve_planar(const Workspace &w, int rows, int cols, int m, const gz_energy *en, const gz_sched *sc,
-                 const int32_t *lo, const int32_t *hi, int32_t *labels_out, gz_stats *st, cudaStream_t s) {
+                 const int32_t *lo, const int32_t *hi, int32_t *labels_out, gz_stats *st, cudaStream_t s,
+                 int hcap = HARD_CAP_DEFAULT) {
     Prob p;
     memset(&p, 0, sizeof(p));
     p.Y = rows; p.G = cols; p.M = m; p.L = m - 1; p.P = rows * cols;
     p.pen = en->penalty; p.inh = en->inhibit; p.hard = en->hard_inhibit ? 1 : 0;
+    p.hcap = hcap;
     p.K = sc && sc->rounds_per_sweep > 0 ? sc->rounds_per_sweep : 12;
     p.bfs_cap = sc ? sc->bfs_cap : 0;
     p.max_sweeps = sc ? sc->max_sweeps : 0;
     p.no_wave = sc ? (sc->flags & GZ_SCHED_NO_WAVE) : 0;
     p.capped = sc ? ((sc->flags & GZ_SCHED_CAPPED) != 0) : 0;
+    {
+        const char *wd = getenv("GZ_WATCHDOG_MS");
+        p.watchdog_ns = (unsigned long long)(wd ? atof(wd) : 20000.0) * 1000000ull;
+    }
     p.lo = lo; p.hi = hi;
     p.vol = w.vol; p.cu = w.cu; p.ph = w.ph; p.pv = w.pv; p.dar = w.dar; p.dbr = w.dbr; p.dad = w.dad; p.dbd = w.dbd;
     p.e = w.e; p.ein = w.ein; p.h = w.h; p.h2 = w.h2; p.reach = w.reach; p.reach2 = w.reach2; p.labels = w.labels;
@@ -759,15 +861,67 @@ int solve_planar(const Workspace &w, int rows, int cols, int m, const gz_energy 
     CK(cudaEventCreate(&e1));
     CK(cudaEventRecord(e0, s));
     const bool win = lo != nullptr;
-    const void *kern = win ? (const void *)gz_solve_kernel<true> : (const void *)gz_solve_kernel<false>;
+    const int NW = words_for(m);
+    const bool det = p.capped != 0;
+    const int which = choose_solver(m, sc);
+    const bool v1 = which == 1;
+    if (!v1 && p.bfs_cap == 0) p.bfs_cap = 64;          // default: BFS at least 64 levels deep per sweep
+    if (!v1 && p.bfs_cap < 0) p.bfs_cap = 0;            // exhaustive BFS every sweep
+    const void *kern = nullptr;
+#define GZ_PICK(W_, NW_, D_) if (win == W_ && NW == NW_ && det == D_) kern = (const void *)gz2::gz_bitsolve_kernel<W_, NW_, D_>;
+#define GZ_PICK_NW(NW_) GZ_PICK(false, NW_, false) GZ_PICK(false, NW_, true) GZ_PICK(true, NW_, false) GZ_PICK(true, NW_, true)
+    const int LPn = lanes_for(m);
+    if (which == 3) {
+        if (LPn == 16) kern = win ? (const void *)gz3::gz_warpsolve_kernel<16, true> : (const void *)gz3::gz_warpsolve_kernel<16, false>;
+        else kern = win ? (const void *)gz3::gz_warpsolve_kernel<32, true> : (const void *)gz3::gz_warpsolve_kernel<32, false>;
+    } else if (which == 2) {
+        GZ_PICK_NW(1) GZ_PICK_NW(2) GZ_PICK_NW(4) GZ_PICK_NW(8)
+    } else {
+        kern = win ? (const void *)gz_solve_kernel<true> : (const void *)gz_solve_kernel<false>;
+    }
+#undef GZ_PICK_NW
+#undef GZ_PICK
+    if (!v1) CK(cudaMemsetAsync(w.bits_base, 0, w.bits_bytes, s));
     int grid = 0;
     int rc = coop_grid(kern, 256, &grid);
     if (rc) return rc;
     const int need = (p.P + 255) / 256;
     if (grid > need) grid = need < 1 ? 1 : need;
-    void *args[] = {&p};
-    CK(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(256), args, 0, s));
+    if (which == 3) {
+        int dev = 0, sms = 0, occ = 0;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0));
+        grid = sms * occ;   // warp groups are grid-strided: use every resident slot
+    }
+    if (getenv("GZ_DEBUG_PROGRESS")) {
+        static unsigned *prog = nullptr;
+        if (!prog) CK(cudaHostAlloc((void **)&prog, 65536 * sizeof(unsigned), cudaHostAllocMapped));
+        memset(prog, 0, 65536 * sizeof(unsigned));
+        unsigned *dprog = nullptr;
+        CK(cudaHostGetDevicePointer((void **)&dprog, prog, 0));
+        p.progress = dprog;
+    }
+    gz2::Bits2 bb = w.bits;
+    gz3::Arr3 a3{w.vol, w.cu, w.ph, w.pv, w.dar, w.dbr, w.dad, w.dbd, w.e, w.ein, w.h2, w.h, w.IN0, w.IN1};
+    void *args1[] = {&p};
+    void *args2[] = {&p, &bb};
+    void *args3[] = {&p, &bb, &a3};
+    CK(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(256), which == 1 ? args1 : (which == 2 ? args2 : args3), 0, s));
     CK(cudaEventRecord(e1, s));
+    if (p.progress) {   // debug: poll instead of blocking, report where blocks stall
+        const double limit = atof(getenv("GZ_DEBUG_PROGRESS"));
+        const double t0 = (double)clock() / CLOCKS_PER_SEC;
+        while (cudaEventQuery(e1) == cudaErrorNotReady) {
+            if ((double)clock() / CLOCKS_PER_SEC - t0 > limit) {
+                fprintf(stderr, "gazecut_b200: solve still running after %.1fs; per-block phase counters:\n", limit);
+                for (int i = 0; i < grid; ++i) fprintf(stderr, "%u%c", p.progress[i], (i % 32 == 31) ? '\n' : ' ');
+                fprintf(stderr, "\n");
+                fflush(stderr);
+                _exit(3);
+            }
+        }
+    }
     unsigned long long h_ctr[gz::CTR_COUNT];
     CK(cudaMemcpyAsync(h_ctr, w.ctr, sizeof(h_ctr), cudaMemcpyDeviceToHost, s));
     if (labels_out && labels_out != w.labels)
@@ -782,7 +936,7 @@ int solve_planar(const Workspace &w, int rows, int cols, int m, const gz_energy 
         memset(st, 0, sizeof(*st));
         st->flow = (int64_t)h_ctr[CTR_FLOW];
         if (p.hard) {   // rescale uncuttable multiples to the reference's 2^56 (see gz_graph.cuh)
-            const int64_t k = st->flow / HARD_CAP, f = st->flow % HARD_CAP;
+            const int64_t k = st->flow / p.hcap, f = st->flow % p.hcap;
             st->flow = k * (int64_t)gz::UNCUTTABLE + f;
         }
         st->const_offset = (int64_t)h_ctr[CTR_OFFSET];
@@ -798,6 +952,7 @@ int solve_planar(const Workspace &w, int rows, int cols, int m, const gz_energy 
         st->reach_passes = (int32_t)h_ctr[CTR_REACH_PASSES];
         st->pulses = (int32_t)h_ctr[CTR_PULSES];
         st->ms_total = ms;
+        for (int q = 0; q < 6; ++q) st->ms_phase[q] = (float)(h_ctr[CTR_T0 + q] * 1e-6);
     }
     return GZ_OK;
 }
@@ -825,7 +980,7 @@ int gz_sad_volume(const uint8_t *left, const uint8_t *right, int32_t img_h, int3
     if (!cb || !left || !right || !vol_out || channels < 1) return GZ_ERR_ARG;
     if (cb->y_min < 0 || cb->y_min + cb->y_extent > img_h || cb->g_extent < 1 || cb->m < 1) return GZ_ERR_ARG;
     const int P = cb->y_extent * cb->g_extent;
-    k_sad<false><<<(P + 127) / 128, 128, 0, (cudaStream_t)stream>>>(left, right, img_w, channels, *cb, vol_out);
+    k_sad<0><<<(P + 127) / 128, 128, 0, (cudaStream_t)stream>>>(left, right, img_w, channels, *cb, vol_out);
     CK(cudaGetLastError());
     return GZ_OK;
 }
@@ -841,7 +996,13 @@ int gz_solve_volume(const int32_t *vol, int32_t rows, int32_t cols, int32_t m, c
     cudaStream_t s = (cudaStream_t)stream;
     Workspace w = carve(workspace, rows, cols, m);
     const int P = rows * cols;
-    k_to_planar<<<(P + 255) / 256, 256, 0, s>>>(vol, P, m, w.vol);
+    if (choose_solver(m, sched) == 3) {
+        const long long n = (long long)P * lanes_for(m);
+        if (lanes_for(m) == 16) k_to_colmajor<16><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(vol, P, m, w.vol);
+        else k_to_colmajor<32><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(vol, P, m, w.vol);
+    } else {
+        k_to_planar<<<(P + 255) / 256, 256, 0, s>>>(vol, P, m, w.vol);
+    }
     CK(cudaGetLastError());
     if (m == 1) {
         // single label: everything folds into the offset (flownet.py:305-322)
@@ -861,7 +1022,25 @@ int gz_solve_volume(const int32_t *vol, int32_t rows, int32_t cols, int32_t m, c
         }
         return GZ_OK;
     }
-    return solve_planar(w, rows, cols, m, energy, sched, lo, hi, labels_out, stats_out, s);
+    // int32 device state: the total source capacity bounds every excess,
+    // residual and flow value, so it must fit (and picks the hard stand-in)
+    CK(cudaMemsetAsync(w.ctr, 0, 16, s));
+    k_source_caps<<<(P + 255) / 256, 256, 0, s>>>(vol, rows, cols, m, lo, hi, *energy, w.ctr);
+    CK(cudaGetLastError());
+    unsigned long long census[2];
+    CK(cudaMemcpyAsync(census, w.ctr, 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const unsigned long long lim = 0x7fffffffull;
+    int hcap = HARD_CAP_DEFAULT;
+    if (energy->hard_inhibit) {
+        unsigned long long hc = 1ull << 16;
+        while (hc <= census[0]) hc <<= 1;
+        if (census[0] >= lim || (census[1] + 1) * hc + census[0] >= lim) return GZ_ERR_OVERFLOW;
+        hcap = (int)hc;
+    } else if (census[0] >= lim) {
+        return GZ_ERR_OVERFLOW;
+    }
+    return solve_planar(w, rows, cols, m, energy, sched, lo, hi, labels_out, stats_out, s, hcap);
 }
 
 int gz_solve_pairs(const uint8_t *left, const uint8_t *right, int32_t batch, int32_t img_h, int32_t img_w,
@@ -879,10 +1058,19 @@ int gz_solve_pairs(const uint8_t *left, const uint8_t *right, int32_t batch, int
     Workspace w = carve(workspace, rows, cols, m);
     const size_t img = (size_t)img_h * img_w * channels;
     for (int b = 0; b < batch; ++b) {
-        k_sad<true><<<(P + 127) / 128, 128, 0, s>>>(left + b * img, right + b * img, img_w, channels, *cb, w.vol);
+        const int which = choose_solver(m, sched);
+        if (which == 3 && lanes_for(m) == 16)
+            k_sad<2, 16><<<(P + 127) / 128, 128, 0, s>>>(left + b * img, right + b * img, img_w, channels, *cb, w.vol);
+        else if (which == 3)
+            k_sad<2, 32><<<(P + 127) / 128, 128, 0, s>>>(left + b * img, right + b * img, img_w, channels, *cb, w.vol);
+        else
+            k_sad<1><<<(P + 127) / 128, 128, 0, s>>>(left + b * img, right + b * img, img_w, channels, *cb, w.vol);
         CK(cudaGetLastError());
+        // SAD costs are <= 255*channels, which bounds the total source capacity
+        const unsigned long long fin = (unsigned long long)P * 255ull * (unsigned long long)channels;
+        if (fin >= (energy->hard_inhibit ? (1ull << 29) : 0x7fffffffull)) return GZ_ERR_OVERFLOW;
         rc = solve_planar(w, rows, cols, m, energy, sched, nullptr, nullptr, labels_out + (size_t)b * P,
-                          stats_out ? stats_out + b : nullptr, s);
+                          stats_out ? stats_out + b : nullptr, s, 1 << 30);
         if (rc) return rc;
         if (stats_out && stats_out[b].energy != stats_out[b].labeling_energy) return GZ_ERR_CONSISTENCY;
     }
