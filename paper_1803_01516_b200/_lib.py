@@ -25,6 +25,7 @@ GZ_SCHED_NO_WAVE = 1
 GZ_SCHED_CAPPED = 2
 GZ_SCHED_V1 = 4
 GZ_SCHED_V2 = 8
+GZ_SCHED_V3 = 16
 
 
 class Cuboid(C.Structure):

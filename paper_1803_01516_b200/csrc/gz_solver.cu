@@ -602,6 +602,7 @@ __global__ void __launch_bounds__(256) gz_solve_kernel(Prob p) {
 
 #include "gz_bitsolve.cuh"
 #include "gz_warpsolve.cuh"
+#include "gz_tilesolve.cuh"
 
 namespace {
 
@@ -814,23 +815,45 @@ Workspace carve(void *ws, int rows, int cols, int m) {
         }                                                                                      \
     } while (0)
 
-int coop_grid(const void *kernel, int threads, int *grid_out) {
+int coop_grid(const void *kernel, int threads, int *grid_out, size_t dyn_smem = 0) {
     int dev = 0, sms = 0, occ = 0;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, dyn_smem));
     if (occ < 1) return GZ_ERR_CUDA;
     *grid_out = sms * occ;
     return GZ_OK;
 }
 
 // 1: v1 column relaxation, 2: bit-parallel (any m <= 256, deterministic
-// relabel when capped), 3: warp-per-chain (m <= 32, exact / uncapped)
+// relabel when capped), 3: warp-per-chain (m <= 32), 4: tile-owned
+// warp-per-chain with temporally blocked BFS (m <= 32, exact / uncapped; default)
 int choose_solver(int m, const gz_sched *sc) {
     const int flags = sc ? sc->flags : 0;
     if ((flags & GZ_SCHED_V1) || words_for(m) == 0) return 1;
     if ((flags & GZ_SCHED_V2) || (flags & GZ_SCHED_CAPPED) || lanes_for(m) == 0) return 2;
-    return 3;
+    if (flags & GZ_SCHED_V3) return 3;
+    return 4;
+}
+
+// Tile geometry of the v4 solver for a team of nb CTAs.
+gz4::Geo tile_geo(int rows, int cols, int nb) {
+    gz4::Geo g;
+    const char *hs = getenv("GZ_BFS_H");
+    g.H = hs ? atoi(hs) : 8;
+    g.TX = 32;
+    // the smallest region (one tile row plus halo) must fit the BFS register tiles
+    while (g.H > 1 && (1 + 2 * g.H) * (g.TX + 2 * g.H) > gz4::SPT * gz4::BLOCK) --g.H;
+    if (g.H < 1) g.H = 1;
+    g.nx = (cols + g.TX - 1) / g.TX;
+    int tile_rows = nb / g.nx;
+    if (tile_rows < 1) tile_rows = 1;
+    g.TY = (rows + tile_rows - 1) / tile_rows;
+    const int rw = cols < g.TX + 2 * g.H ? cols : g.TX + 2 * g.H;
+    while (g.TY > 1 && (rows < g.TY + 2 * g.H ? rows : g.TY + 2 * g.H) * rw > gz4::SPT * gz4::BLOCK) --g.TY;
+    g.ny = (rows + g.TY - 1) / g.TY;
+    g.ntiles = g.nx * g.ny;
+    return g;
 }
 
 // Solve one problem whose volume is already in w.vol (layout of the chosen solver).
@@ -865,13 +888,16 @@ int solve_planar(const Workspace &w, int rows, int cols, int m, const gz_energy 
     const bool det = p.capped != 0;
     const int which = choose_solver(m, sc);
     const bool v1 = which == 1;
-    if (!v1 && p.bfs_cap == 0) p.bfs_cap = 64;          // default: BFS at least 64 levels deep per sweep
+    if (!v1 && p.bfs_cap == 0) p.bfs_cap = which == 4 ? 48 : 64;   // default: BFS depth before it may stop at excess
     if (!v1 && p.bfs_cap < 0) p.bfs_cap = 0;            // exhaustive BFS every sweep
     const void *kern = nullptr;
 #define GZ_PICK(W_, NW_, D_) if (win == W_ && NW == NW_ && det == D_) kern = (const void *)gz2::gz_bitsolve_kernel<W_, NW_, D_>;
 #define GZ_PICK_NW(NW_) GZ_PICK(false, NW_, false) GZ_PICK(false, NW_, true) GZ_PICK(true, NW_, false) GZ_PICK(true, NW_, true)
     const int LPn = lanes_for(m);
-    if (which == 3) {
+    if (which == 4) {
+        if (LPn == 16) kern = win ? (const void *)gz4::gz_tilesolve_kernel<16, true> : (const void *)gz4::gz_tilesolve_kernel<16, false>;
+        else kern = win ? (const void *)gz4::gz_tilesolve_kernel<32, true> : (const void *)gz4::gz_tilesolve_kernel<32, false>;
+    } else if (which == 3) {
         if (LPn == 16) kern = win ? (const void *)gz3::gz_warpsolve_kernel<16, true> : (const void *)gz3::gz_warpsolve_kernel<16, false>;
         else kern = win ? (const void *)gz3::gz_warpsolve_kernel<32, true> : (const void *)gz3::gz_warpsolve_kernel<32, false>;
     } else if (which == 2) {
@@ -882,11 +908,16 @@ int solve_planar(const Workspace &w, int rows, int cols, int m, const gz_energy 
 #undef GZ_PICK_NW
 #undef GZ_PICK
     if (!v1) CK(cudaMemsetAsync(w.bits_base, 0, w.bits_bytes, s));
+    const int threads = which == 4 ? gz4::BLOCK : 256;
+    const size_t dyn_smem = which == 4 ? 2 * gz4::SPT * gz4::BLOCK * sizeof(uint32_t) : 0;
     int grid = 0;
-    int rc = coop_grid(kern, 256, &grid);
+    int rc = coop_grid(kern, threads, &grid, dyn_smem);
     if (rc) return rc;
     const int need = (p.P + 255) / 256;
     if (grid > need) grid = need < 1 ? 1 : need;
+    gz4::Geo geo{};
+    unsigned *bar = (unsigned *)(w.ctr + gz::CTR_BAR);
+    if (which == 4) geo = tile_geo(rows, cols, grid);
     if (which == 3) {
         int dev = 0, sms = 0, occ = 0;
         CK(cudaGetDevice(&dev));
@@ -907,7 +938,14 @@ int solve_planar(const Workspace &w, int rows, int cols, int m, const gz_energy 
     void *args1[] = {&p};
     void *args2[] = {&p, &bb};
     void *args3[] = {&p, &bb, &a3};
-    CK(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(256), which == 1 ? args1 : (which == 2 ? args2 : args3), 0, s));
+    void *args4[] = {&p, &bb, &a3, &geo, &bar};
+    if (which == 4) {
+        if (geo.ntiles < grid) grid = geo.ntiles;   // every CTA owns at least one tile
+        geo = tile_geo(rows, cols, grid);
+        CK(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(threads), args4, dyn_smem, s));
+    } else {
+        CK(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(256), which == 1 ? args1 : (which == 2 ? args2 : args3), 0, s));
+    }
     CK(cudaEventRecord(e1, s));
     if (p.progress) {   // debug: poll instead of blocking, report where blocks stall
         const double limit = atof(getenv("GZ_DEBUG_PROGRESS"));
@@ -996,7 +1034,7 @@ int gz_solve_volume(const int32_t *vol, int32_t rows, int32_t cols, int32_t m, c
     cudaStream_t s = (cudaStream_t)stream;
     Workspace w = carve(workspace, rows, cols, m);
     const int P = rows * cols;
-    if (choose_solver(m, sched) == 3) {
+    if (choose_solver(m, sched) >= 3) {
         const long long n = (long long)P * lanes_for(m);
         if (lanes_for(m) == 16) k_to_colmajor<16><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(vol, P, m, w.vol);
         else k_to_colmajor<32><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(vol, P, m, w.vol);
@@ -1059,9 +1097,9 @@ int gz_solve_pairs(const uint8_t *left, const uint8_t *right, int32_t batch, int
     const size_t img = (size_t)img_h * img_w * channels;
     for (int b = 0; b < batch; ++b) {
         const int which = choose_solver(m, sched);
-        if (which == 3 && lanes_for(m) == 16)
+        if (which >= 3 && lanes_for(m) == 16)
             k_sad<2, 16><<<(P + 127) / 128, 128, 0, s>>>(left + b * img, right + b * img, img_w, channels, *cb, w.vol);
-        else if (which == 3)
+        else if (which >= 3)
             k_sad<2, 32><<<(P + 127) / 128, 128, 0, s>>>(left + b * img, right + b * img, img_w, channels, *cb, w.vol);
         else
             k_sad<1><<<(P + 127) / 128, 128, 0, s>>>(left + b * img, right + b * img, img_w, channels, *cb, w.vol);
@@ -1146,6 +1184,6 @@ const char *gz_status_string(int status) {
     return "unknown status";
 }
 
-const char *gz_build_info(void) { return "gazecut_b200 v1 sm_100a persistent-cooperative push-relabel"; }
+const char *gz_build_info(void) { return "gazecut_b200 v4 sm_100a tile-owned persistent push-relabel (temporally blocked BFS)"; }
 
 }  // extern "C"

@@ -46,13 +46,13 @@ struct Lane {
     bool valid, real;
     int nc[4], nlo[4], nhi[4];
     bool has[4];
-    __device__ __forceinline__ void init(const Prob &p, int group) {
-        constexpr int CPW = 32 / LP;
+    // sites c_base .. c_base + nsites - 1 (nsites <= 32 / LP), one per LP-lane segment
+    __device__ __forceinline__ void init(const Prob &p, int c_base, int nsites) {
         const int lane = threadIdx.x & 31;
-        c = group * CPW + lane / LP;
+        c = c_base + lane / LP;
         j = lane % LP;
         t = j + 1;
-        valid = c < p.P;
+        valid = lane / LP < nsites && c < p.P;
         const int cc = valid ? c : 0;
         y = cc / p.G;
         g = cc - y * p.G;
@@ -173,10 +173,10 @@ __device__ __forceinline__ uint32_t seg_ballot(bool pred) {
 // ---------------------------------------------------------------------------
 // init: residuals from the volume, source saturation, chain wave, offset
 template <int LP, bool WIN>
-__device__ void w_init(const Prob &p, const Arr3 &a, const Bits2 &b, int group, long long &flow, long long &offset,
-                       long long &presat) {
+__device__ void w_init(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base, int nsites, long long &flow,
+                       long long &offset, long long &presat) {
     Lane<LP, WIN> L;
-    L.init(p, group);
+    L.init(p, c_base, nsites);
     const int I = L.I;
     const int volj = (L.valid && L.j < p.M) ? a.vol[I] : 0;
     const int vol_above = from_above<LP>(volj);
@@ -239,9 +239,9 @@ __device__ void w_init(const Prob &p, const Arr3 &a, const Bits2 &b, int group, 
 // ---------------------------------------------------------------------------
 // mask build (ballots) + pending inbox merge + BFS reset
 template <int LP, bool WIN>
-__device__ void w_build(const Prob &p, const Arr3 &a, const Bits2 &b, int group) {
+__device__ void w_build(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base, int nsites) {
     Lane<LP, WIN> L;
-    L.init(p, group);
+    L.init(p, c_base, nsites);
     const int I = L.I, P = p.P;
     // merge both inbox buffers (the last pulse's lateral pushes)
     uint32_t in0 = L.valid ? a.IN0[L.c] : 0u, in1 = L.valid ? a.IN1[L.c] : 0u;
@@ -313,10 +313,10 @@ __device__ int w_bfs_level(const Prob &p, const Arr3 &a, const Bits2 &b, int c, 
 // ---------------------------------------------------------------------------
 // one pulse on a warp group of chains
 template <int LP, bool WIN>
-__device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int group, int parity, long long &flow,
-                        long long &pushes, long long &relabels) {
+__device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base, int nsites, int parity,
+                        long long &flow, long long &pushes, long long &relabels) {
     Lane<LP, WIN> L;
-    L.init(p, group);
+    L.init(p, c_base, nsites);
     const int I = L.I;
     uint32_t *IN_prev = parity ? a.IN0 : a.IN1;
     uint32_t *IN_cur = parity ? a.IN1 : a.IN0;
@@ -349,7 +349,7 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int group,
     }
     // lateral and downward pushes of the remaining excess
     int dn = 0;
-    int ph_d = 0, pv_d = 0, dar_d = 0, dbr_d = 0, dad_d = 0, dbd_d = 0;
+    int ph_d = 0, pv_d = 0, dar_d = 0, dad_d = 0;
     int phL_d = 0, pvU_d = 0, dbrL_d = 0, dbdU_d = 0, dbr_up_d = 0, darL_up_d = 0, dbd_up_d = 0, dadU_up_d = 0;
     if (live && e > 0) {
 #pragma unroll
@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(256) gz_warpsolve_kernel(Prob p, Bits2 b, Arr3
 #define FOR_GROUPS for (int it_ = 0, grp = wid; it_ < giter; ++it_, grp += nwarps) if (grp < ngroups)
 
     PROG();
-    FOR_GROUPS w_init<LP, WIN>(p, a, b, grp, flow, offset, presat);
+    FOR_GROUPS w_init<LP, WIN>(p, a, b, grp * CPW, CPW, flow, offset, presat);
     PROG();
     grid.sync();
     TICK(0);
@@ -481,7 +481,7 @@ __global__ void __launch_bounds__(256) gz_warpsolve_kernel(Prob p, Bits2 b, Arr3
     bool err = false;
     const int bfs_min = p.bfs_cap > 0 ? p.bfs_cap : (1 << 30);
     for (;;) {
-        FOR_GROUPS w_build<LP, WIN>(p, a, b, grp);
+        FOR_GROUPS w_build<LP, WIN>(p, a, b, grp * CPW, CPW);
         PROG();
         grid.sync();
         TICK(1);
@@ -508,7 +508,7 @@ __global__ void __launch_bounds__(256) gz_warpsolve_kernel(Prob p, Bits2 b, Arr3
         FOR_COLS b.A[c] = b.V[c] & b.EX[c];
         grid.sync();
         for (int pulse = 0; pulse < p.K; ++pulse) {
-            FOR_GROUPS w_pulse<LP, WIN>(p, a, b, grp, parity, flow, pushes, relabels);
+            FOR_GROUPS w_pulse<LP, WIN>(p, a, b, grp * CPW, CPW, parity, flow, pushes, relabels);
             PROG();
             grid.sync();
             parity ^= 1;
