@@ -74,6 +74,7 @@ typedef struct {
 typedef struct {
     int64_t flow, energy, const_offset, nodes, arcs, presaturated, pushes, relabels;
     int64_t labeling_energy;       /* energy.py:129-155 recomputed on device */
+    int64_t node_updates;          /* node updates done by push/relabel pulses (v4; roofline units) */
     int32_t sweeps, converged, stranded_excess_nodes, bfs_passes, reach_passes, pulses;
     float ms_total;                /* device time of the solve (CUDA events) */
     float ms_phase[6];             /* in-kernel phase times: init, mask build, global relabel, pulses,

@@ -45,7 +45,7 @@ class Sched(C.Structure):
 class Stats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in
                 ("flow", "energy", "const_offset", "nodes", "arcs", "presaturated", "pushes",
-                 "relabels", "labeling_energy")] + \
+                 "relabels", "labeling_energy", "node_updates")] + \
                [(n, C.c_int32) for n in
                 ("sweeps", "converged", "stranded_excess_nodes", "bfs_passes", "reach_passes",
                  "pulses")] + \

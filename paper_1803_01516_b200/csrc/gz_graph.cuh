@@ -75,6 +75,7 @@ enum Ctr : int {
     CTR_FLAG0 = 16,     // 3 rotating "changed" flags
     CTR_ACT0 = 20,      // 3 rotating active counters
     CTR_T0 = 24,        // 6 phase timers (ns): init, mask build, bfs, pulses, reach, tail
+    CTR_UPDATES = 30,   // node updates performed by pulses (v4)
     CTR_BAR = 31,       // team barrier arrival counter (v4)
     CTR_COUNT = 32
 };

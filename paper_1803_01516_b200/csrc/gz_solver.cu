@@ -982,6 +982,7 @@ int solve_planar(const Workspace &w, int rows, int cols, int m, const gz_energy 
         st->pushes = (int64_t)h_ctr[CTR_PUSHES];
         st->relabels = (int64_t)h_ctr[CTR_RELABELS];
         st->labeling_energy = h_ctr[CTR_HARDVIOL] ? (int64_t)gz::UNCUTTABLE : (int64_t)h_ctr[CTR_ENERGY];
+        st->node_updates = (int64_t)h_ctr[CTR_UPDATES];
         st->converged = (int32_t)h_ctr[CTR_CONVERGED];
         st->energy = st->converged ? st->flow + st->const_offset : st->labeling_energy;
         st->sweeps = (int32_t)h_ctr[CTR_SWEEPS];

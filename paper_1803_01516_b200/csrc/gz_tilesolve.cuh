@@ -198,11 +198,14 @@ __global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b,
     const int ngroups = (p.P + CPW - 1) / CPW;
     const int gnw = tm.nb * nwarps, gwid = tm.rank * nwarps + warp;
     const int giter = (ngroups + gnw - 1) / gnw;
+    const int ttid = tm.rank * blockDim.x + threadIdx.x, tstride = tm.nb * blockDim.x;
+    long long updates = 0;   // groups processed by pulses (x CPW x L = node updates)
 
     FOR_TILES {
         const TileBox tb(p, g, tile);
         for_tile_groups<LP>(p, tb, [&](int cb, int ns) { gz3::w_init<LP, WIN>(p, a, b, cb, ns, flow, offset, presat); });
     }
+    for (int c = ttid; c < p.P; c += tstride) b.IN[c] = 1u;   // every site starts dirty
     tm.sync();
     TICK(0);
     int sweeps = 0, levels_total = 0, pulses = 0, rot = 0, parity = 0;
@@ -210,9 +213,35 @@ __global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b,
     bool err = false;
     const int bfs_min = p.bfs_cap > 0 ? p.bfs_cap : (1 << 30);
     for (;;) {
-        FOR_TILES {
-            const TileBox tb(p, g, tile);
-            for_tile_groups<LP>(p, tb, [&](int cb, int ns) { gz3::w_build<LP, WIN>(p, a, b, cb, ns); });
+        // ---- sweep set-up: bulk coalesced resets, then arc masks of dirty sites only ----
+        for (int c = ttid; c < p.P; c += tstride) {
+            const int hi = WIN ? p.hi[c] : p.L;
+            b.F0[c] = BW<1>::range(hi, p.M).w[0];
+            b.V[c] = 0u;
+        }
+        {
+            const int4 hinf4 = make_int4(HINF, HINF, HINF, HINF);
+            int4 *h4 = reinterpret_cast<int4 *>(a.h);
+            const int n4 = p.P * (LP / 4);
+            for (int q = ttid; q < n4; q += tstride) h4[q] = hinf4;
+        }
+        for (int it0 = 0; it0 < giter; it0 += 32) {
+            const int it = it0 + lane;
+            const int grp = gwid + it * gnw;
+            uint32_t wk = 0u;
+            if (it < giter && grp < ngroups) {
+                const int c0 = grp * CPW;
+                wk = b.IN[c0];
+                if (CPW == 2 && c0 + 1 < p.P) wk |= b.IN[c0 + 1];
+            }
+            uint32_t msk = __ballot_sync(FULL, wk != 0u);
+            while (msk) {
+                const int k = __ffs(msk) - 1;
+                msk &= msk - 1;
+                const int c0 = (gwid + (it0 + k) * gnw) * CPW;
+                gz3::w_build<LP, WIN, false>(p, a, b, c0, CPW);
+                if (lane < CPW && c0 + lane < p.P) b.IN[c0 + lane] = 0u;
+            }
         }
         tm.sync();
         TICK(1);
@@ -267,11 +296,12 @@ __global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b,
                     if (CPW == 2 && c0 + 1 < p.P) wk |= b.A[c0 + 1] | IN_prev[c0 + 1];
                 }
                 uint32_t msk = __ballot_sync(FULL, wk != 0u);
+                updates += __popc(msk);
                 while (msk) {
                     const int k = __ffs(msk) - 1;
                     msk &= msk - 1;
                     const int g2 = gwid + (it0 + k) * gnw;
-                    gz3::w_pulse<LP, WIN>(p, a, b, g2 * CPW, CPW, parity, flow, pushes, relabels);
+                    gz3::w_pulse<LP, WIN, false>(p, a, b, g2 * CPW, CPW, parity, flow, pushes, relabels, b.IN);
                 }
             }
             tm.sync();
@@ -333,6 +363,7 @@ __global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b,
     warp_add_u64(&p.ctr[CTR_RELABELS], relabels);
     warp_add_u64(&p.ctr[CTR_ENERGY], energy);
     warp_add_u64(&p.ctr[CTR_STRANDED], stranded);
+    if (lane == 0 && updates) atomicAdd(&p.ctr[CTR_UPDATES], (unsigned long long)updates * CPW * p.L);
     if (viol) p.ctr[CTR_HARDVIOL] = 1;
     if (threadIdx.x == 0 && tm.rank == 0) {
         p.ctr[CTR_SWEEPS] = sweeps;

@@ -238,24 +238,27 @@ __device__ void w_init(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base,
 
 // ---------------------------------------------------------------------------
 // mask build (ballots) + pending inbox merge + BFS reset
-template <int LP, bool WIN>
+template <int LP, bool WIN, bool RESET_H = true>
 __device__ void w_build(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base, int nsites) {
     Lane<LP, WIN> L;
     L.init(p, c_base, nsites);
     const int I = L.I, P = p.P;
-    // merge both inbox buffers (the last pulse's lateral pushes)
-    uint32_t in0 = L.valid ? a.IN0[L.c] : 0u, in1 = L.valid ? a.IN1[L.c] : 0u;
+    // every global load of the group is issued before the first store (one
+    // round trip): inbox words and values, excess, then the arc state
+    const uint32_t in0 = L.valid ? a.IN0[L.c] : 0u, in1 = L.valid ? a.IN1[L.c] : 0u;
     int e = L.valid ? a.e[I] : 0;
-    if ((in0 >> L.j) & 1u) { e += a.ein0[I]; a.ein0[I] = 0; }
-    if ((in1 >> L.j) & 1u) { e += a.ein1[I]; a.ein1[I] = 0; }
-    if (L.valid && ((in0 | in1) >> L.j) & 1u) a.e[I] = e;
+    const int x0 = L.valid ? a.ein0[I] : 0, x1 = L.valid ? a.ein1[I] : 0;
     Arcs<LP, WIN> R;
     R.load(p, a, L);
+    // merge both inbox buffers (the last pulse's lateral pushes)
+    if ((in0 >> L.j) & 1u) { e += x0; a.ein0[I] = 0; }
+    if ((in1 >> L.j) & 1u) { e += x1; a.ein1[I] = 0; }
+    if (L.valid && ((in0 | in1) >> L.j) & 1u) a.e[I] = e;
     uint32_t m[13];
 #pragma unroll
     for (int q = 0; q < 13; ++q) m[q] = seg_ballot<LP>(L.real && R.r[q] > 0);
     const uint32_t ex = seg_ballot<LP>(L.real && e > 0);
-    if (L.valid) a.h[I] = HINF;
+    if (RESET_H && L.valid) a.h[I] = HINF;
     if (L.valid && L.j == 0) {
 #pragma unroll
         for (int q = 0; q < 13; ++q) b.mask[(size_t)q * P + L.c] = m[q];
@@ -312,9 +315,9 @@ __device__ int w_bfs_level(const Prob &p, const Arr3 &a, const Bits2 &b, int c, 
 
 // ---------------------------------------------------------------------------
 // one pulse on a warp group of chains
-template <int LP, bool WIN>
+template <int LP, bool WIN, bool CHECK_IDLE = true>
 __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base, int nsites, int parity,
-                        long long &flow, long long &pushes, long long &relabels) {
+                        long long &flow, long long &pushes, long long &relabels, uint32_t *dirty = nullptr) {
     Lane<LP, WIN> L;
     L.init(p, c_base, nsites);
     const int I = L.I;
@@ -323,12 +326,15 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
     int32_t *ein_prev = parity ? a.ein0 : a.ein1;
     int32_t *ein_cur = parity ? a.ein1 : a.ein0;
     const uint32_t act = L.valid ? b.A[L.c] : 0u, inb = L.valid ? IN_prev[L.c] : 0u;
-    if (!__any_sync(FULL, (act | inb) != 0u)) return;
+    if (CHECK_IDLE && !__any_sync(FULL, (act | inb) != 0u)) return;
+    // all loads before the first store: one round trip per group (ein_prev has
+    // no writer during this pulse, so reading it unconditionally is safe)
     int e = L.valid ? a.e[I] : 0;
-    if ((inb >> L.j) & 1u) { e += ein_prev[I]; ein_prev[I] = 0; }
-    if (L.valid && L.j == 0 && inb) IN_prev[L.c] = 0u;
+    const int xin = L.valid ? ein_prev[I] : 0;
     Arcs<LP, WIN> R;
     R.load(p, a, L);
+    if ((inb >> L.j) & 1u) { e += xin; ein_prev[I] = 0; }
+    if (L.valid && L.j == 0 && inb) IN_prev[L.c] = 0u;
     const int hu = R.h_u;
     const bool live = L.real && hu < HINF;
     // upward chain wave through admissible chain arcs
@@ -420,6 +426,17 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
     }
     const uint32_t newA = seg_ballot<LP>(L.real && e > 0 && hnew < HINF);
     if (L.valid && L.j == 0) b.A[L.c] = newA;
+    if (dirty) {
+        // a push changes this site's residuals and the pair state / excess of its
+        // neighbours: all of them need their arc masks rebuilt next sweep
+        const uint32_t pm = seg_ballot<LP>(pushed);
+        if (pm && L.valid && L.j == 0) {
+            dirty[L.c] = 1u;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (L.has[i]) dirty[L.nc[i]] = 1u;
+        }
+    }
 }
 
 // extraction seeds from the last mask build's excess bits

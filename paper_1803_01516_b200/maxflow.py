@@ -95,6 +95,7 @@ def maxflow_push_relabel(net: FlowNetwork, rounds_per_sweep: int = 12, max_sweep
         "bfs_passes": int(st.bfs_passes),
         "reach_passes": int(st.reach_passes),
         "labeling_energy": int(st.labeling_energy),
+        "node_updates": int(st.node_updates),
         "phase_ms": {k: round(float(v), 4) for k, v in
                      zip(("init", "mask_build", "global_relabel", "pulses", "extract", "tail"), st.ms_phase)},
     }

@@ -28,6 +28,7 @@ def _stats_dict(st: _lib.Stats) -> dict:
         "stranded_excess_nodes": int(st.stranded_excess_nodes), "pulses": int(st.pulses),
         "bfs_passes": int(st.bfs_passes), "reach_passes": int(st.reach_passes),
         "device_ms": float(st.ms_total), "labeling_energy": int(st.labeling_energy),
+        "node_updates": int(st.node_updates),
         "phase_ms": {k: round(float(v), 4) for k, v in
                      zip(("init", "mask_build", "global_relabel", "pulses", "extract", "tail"), st.ms_phase)},
     }
