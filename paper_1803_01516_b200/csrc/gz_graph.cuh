@@ -76,8 +76,8 @@ enum Ctr : int {
     CTR_ACT0 = 20,      // 3 rotating active counters
     CTR_T0 = 24,        // 6 phase timers (ns): init, mask build, bfs, pulses, reach, tail
     CTR_UPDATES = 30,   // node updates performed by pulses (v4)
-    CTR_BAR = 31,       // team barrier arrival counter (v4)
-    CTR_COUNT = 32
+    CTR_BAR0 = 32,      // 3 rotating team-barrier words (v4)
+    CTR_COUNT = 40
 };
 
 __host__ __device__ inline size_t plane_elems(int M, int P) { return (size_t)M * (size_t)P; }

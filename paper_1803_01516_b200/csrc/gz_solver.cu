@@ -843,14 +843,14 @@ gz4::Geo tile_geo(int rows, int cols, int nb) {
     g.H = hs ? atoi(hs) : 8;
     g.TX = 32;
     // the smallest region (one tile row plus halo) must fit the BFS register tiles
-    while (g.H > 1 && (1 + 2 * g.H) * (g.TX + 2 * g.H) > gz4::SPT * gz4::BLOCK) --g.H;
+    while (g.H > 1 && (1 + 2 * g.H) * (g.TX + 2 * g.H) > gz4::REGMAX) --g.H;
     if (g.H < 1) g.H = 1;
     g.nx = (cols + g.TX - 1) / g.TX;
     int tile_rows = nb / g.nx;
     if (tile_rows < 1) tile_rows = 1;
     g.TY = (rows + tile_rows - 1) / tile_rows;
     const int rw = cols < g.TX + 2 * g.H ? cols : g.TX + 2 * g.H;
-    while (g.TY > 1 && (rows < g.TY + 2 * g.H ? rows : g.TY + 2 * g.H) * rw > gz4::SPT * gz4::BLOCK) --g.TY;
+    while (g.TY > 1 && (rows < g.TY + 2 * g.H ? rows : g.TY + 2 * g.H) * rw > gz4::REGMAX) --g.TY;
     g.ny = (rows + g.TY - 1) / g.TY;
     g.ntiles = g.nx * g.ny;
     return g;
@@ -909,14 +909,15 @@ int solve_planar(const Workspace &w, int rows, int cols, int m, const gz_energy 
 #undef GZ_PICK
     if (!v1) CK(cudaMemsetAsync(w.bits_base, 0, w.bits_bytes, s));
     const int threads = which == 4 ? gz4::BLOCK : 256;
-    const size_t dyn_smem = which == 4 ? 2 * gz4::SPT * gz4::BLOCK * sizeof(uint32_t) : 0;
+    const size_t dyn_smem = which == 4 ? gz4::SMEM_BYTES : 0;
+    if (which == 4) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem));
     int grid = 0;
     int rc = coop_grid(kern, threads, &grid, dyn_smem);
     if (rc) return rc;
     const int need = (p.P + 255) / 256;
     if (grid > need) grid = need < 1 ? 1 : need;
     gz4::Geo geo{};
-    unsigned *bar = (unsigned *)(w.ctr + gz::CTR_BAR);
+    unsigned long long *bar = w.ctr + gz::CTR_BAR0;
     if (which == 4) geo = tile_geo(rows, cols, grid);
     if (which == 3) {
         int dev = 0, sms = 0, occ = 0;

@@ -31,50 +31,51 @@ using gz3::Arr3;
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int BLOCK = 512;   // threads per CTA (one CTA per SM)
-constexpr int SPT = 4;       // BFS region sites per thread (registers)
+constexpr int SPT = 4;       // BFS region sites per thread
+constexpr int REGMAX = SPT * BLOCK;   // BFS region sites per tile (tile + halo)
+constexpr size_t SMEM_BYTES = (size_t)(2 + 13) * REGMAX * sizeof(uint32_t);   // frontier x2 + arc masks
 
 struct Geo {
     int TY, TX, ny, nx, ntiles, H;
 };
 
+// Team barrier with a fused 2-bit OR reduction.  Barrier k uses word k % 3 of
+// `bar`: each CTA adds, in ONE atomic, its arrival (low 32 bits, generation-flip
+// trick: rank 0 adds 2^31 - (nb-1), the others 1, so bit 31 flips exactly when
+// the last CTA arrives) plus a count of flag-0 / flag-1 CTAs in bits 32-47 /
+// 48-63.  The value a CTA sees when it observes the flip therefore carries the
+// team's OR.  After barrier k every CTA has read word (k-1) % 3, so rank 0
+// clears it for barrier k+2 (nobody reaches k+2 before rank 0 reaches k+1).
 struct Team {
-    unsigned *bar;   // arrival counter of this team
+    unsigned long long *bar;   // 3 rotating words of this team
     int nb, rank;
-    __device__ __forceinline__ void sync() const {
+    __device__ __forceinline__ unsigned sync_or(unsigned flags, int &phase, unsigned *s_f3, unsigned *s_r3) const {
+        const int k3 = phase % 3;
+        const unsigned w = __reduce_or_sync(FULL, flags);
+        if ((threadIdx.x & 31) == 0 && w) atomicOr(&s_f3[k3], w);
         __syncthreads();
         if (threadIdx.x == 0) {
-            const unsigned inc = rank == 0 ? (0x80000000u - (unsigned)(nb - 1)) : 1u;
+            const unsigned f = s_f3[k3];
+            s_f3[(k3 + 1) % 3] = 0u;   // last read two barriers ago
+            const unsigned long long inc = (rank == 0 ? 0x80000000ull - (unsigned long long)(nb - 1) : 1ull) |
+                                           ((f & 1u) ? 1ull << 32 : 0ull) | ((f & 2u) ? 1ull << 48 : 0ull);
+            unsigned long long *word = bar + k3;
             __threadfence();
-            const unsigned old = atomicAdd(bar, inc);
-            while (((old ^ *(volatile unsigned *)bar) & 0x80000000u) == 0u) {
-            }
+            const unsigned long long old = atomicAdd(word, inc);
+            unsigned long long cur;
+            do {
+                cur = *(volatile unsigned long long *)word;
+            } while (((old ^ cur) & 0x80000000ull) == 0ull);
+            if (rank == 0) bar[(k3 + 2) % 3] = 0ull;
             __threadfence();
+            s_r3[k3] = ((cur >> 32) & 0xffffull ? 1u : 0u) | ((cur >> 48) ? 2u : 0u);
         }
         __syncthreads();
+        const unsigned r = s_r3[k3];
+        ++phase;
+        return r;
     }
 };
-
-// team-wide OR of per-thread flag bits (one team barrier); slots rotate over 3
-// entries so a slot is only cleared two calls after its last reader.
-__device__ __forceinline__ unsigned team_or(const Team &tm, unsigned flags, unsigned long long *slots, int &rot,
-                                            unsigned *s_acc3) {
-    unsigned *s_acc = s_acc3 + rot;
-    if (threadIdx.x == 0) *s_acc = 0u;
-    __syncthreads();
-    const unsigned w = __reduce_or_sync(FULL, flags);
-    if ((threadIdx.x & 31) == 0 && w) atomicOr(s_acc, w);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        if (*s_acc) atomicOr(&slots[rot], (unsigned long long)*s_acc);
-        if (tm.rank == 0) slots[(rot + 1) % 3] = 0ull;
-    }
-    tm.sync();
-    if (threadIdx.x == 0) *s_acc = (unsigned)((volatile unsigned long long *)slots)[rot];
-    __syncthreads();
-    const unsigned r = *s_acc;
-    rot = (rot + 1) % 3;
-    return r;
-}
 
 struct TileBox {
     int y0, y1, x0, x1;
@@ -99,16 +100,18 @@ __device__ __forceinline__ void for_tile_groups(const Prob &p, const TileBox &tb
 
 // ---------------------------------------------------------------------------
 // one BFS round on a tile: H levels from depth d.  Returns bit0 = new interior
-// nodes, bit1 = a new interior node holds excess.
+// nodes, bit1 = a new interior node holds excess.  The region's 13 arc-mask
+// words per site live in shared memory (sM, REGMAX stride); they are loaded
+// when load_masks is set -- once per sweep when every CTA owns one tile.
 template <int LP, bool WIN>
 __device__ unsigned bfs_round(const Prob &p, const Arr3 &a, const Bits2 &b, const Geo &g, const TileBox &tb,
                               const uint32_t *Fin, uint32_t *Fout, const uint32_t *Vin, uint32_t *Vout, int d,
-                              uint32_t *sF0, uint32_t *sF1) {
+                              uint32_t *sF0, uint32_t *sF1, uint32_t *sM, bool load_masks) {
     const int P = p.P, H = g.H;
     const int ry0 = max(tb.y0 - H, 0), ry1 = min(tb.y1 + H, p.Y);
     const int rx0 = max(tb.x0 - H, 0), rx1 = min(tb.x1 + H, p.G);
     const int RW = rx1 - rx0, nreg = (ry1 - ry0) * RW;
-    uint32_t M[SPT][13], V[SPT], EX[SPT], RNG[SPT];
+    uint32_t V[SPT], EX[SPT], RNG[SPT];
     int C[SPT];
     bool IN_[SPT];
     unsigned NB[SPT];   // neighbour-in-region bits: right, left, down, up
@@ -122,8 +125,10 @@ __device__ unsigned bfs_round(const Prob &p, const Arr3 &a, const Bits2 &b, cons
         C[k] = ok ? c : -1;
         IN_[k] = ok && y >= tb.y0 && y < tb.y1 && x >= tb.x0 && x < tb.x1;
         NB[k] = (rj + 1 < RW ? 1u : 0u) | (rj > 0 ? 2u : 0u) | (i + RW < nreg ? 4u : 0u) | (ri > 0 ? 8u : 0u);
+        if (load_masks && ok) {
 #pragma unroll
-        for (int q = 0; q < 13; ++q) M[k][q] = ok ? b.mask[(size_t)q * P + c] : 0u;
+            for (int q = 0; q < 13; ++q) sM[q * REGMAX + i] = b.mask[(size_t)q * P + c];
+        }
         V[k] = ok ? Vin[c] : 0u;
         EX[k] = IN_[k] ? b.EX[c] : 0u;
         int lo = 0, hi = p.L;
@@ -144,11 +149,16 @@ __device__ unsigned bfs_round(const Prob &p, const Arr3 &a, const Bits2 &b, cons
             const uint32_t Fn1 = (NB[k] & 2u) ? cur[i - 1] : 0u;
             const uint32_t Fn2 = (NB[k] & 4u) ? cur[i + RW] : 0u;
             const uint32_t Fn3 = (NB[k] & 8u) ? cur[i - RW] : 0u;
-            uint32_t N = (F << 1) | ((F >> 1) & M[k][A_UP]);
-            N |= (Fn0 & M[k][A_SR]) | ((Fn0 << 1) & M[k][A_DR]) | ((Fn0 >> 1) & M[k][A_UR]);
-            N |= (Fn1 & M[k][A_SL]) | ((Fn1 << 1) & M[k][A_DL]) | ((Fn1 >> 1) & M[k][A_UL]);
-            N |= (Fn2 & M[k][A_SD]) | ((Fn2 << 1) & M[k][A_DD]) | ((Fn2 >> 1) & M[k][A_UD]);
-            N |= (Fn3 & M[k][A_SU]) | ((Fn3 << 1) & M[k][A_DU]) | ((Fn3 >> 1) & M[k][A_UU]);
+            if ((F | Fn0 | Fn1 | Fn2 | Fn3) == 0u) {   // no frontier next to this site
+                nxt[i] = 0u;
+                continue;
+            }
+            const uint32_t *m = sM + i;
+            uint32_t N = (F << 1) | ((F >> 1) & m[A_UP * REGMAX]);
+            N |= (Fn0 & m[A_SR * REGMAX]) | ((Fn0 << 1) & m[A_DR * REGMAX]) | ((Fn0 >> 1) & m[A_UR * REGMAX]);
+            N |= (Fn1 & m[A_SL * REGMAX]) | ((Fn1 << 1) & m[A_DL * REGMAX]) | ((Fn1 >> 1) & m[A_UL * REGMAX]);
+            N |= (Fn2 & m[A_SD * REGMAX]) | ((Fn2 << 1) & m[A_DD * REGMAX]) | ((Fn2 >> 1) & m[A_UD * REGMAX]);
+            N |= (Fn3 & m[A_SU * REGMAX]) | ((Fn3 << 1) & m[A_DU * REGMAX]) | ((Fn3 >> 1) & m[A_UU * REGMAX]);
             N &= RNG[k] & ~V[k];
             V[k] |= N;
             nxt[i] = N;
@@ -180,11 +190,17 @@ __device__ unsigned bfs_round(const Prob &p, const Arr3 &a, const Bits2 &b, cons
 
 // ---------------------------------------------------------------------------
 template <int LP, bool WIN>
-__global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b, Arr3 a, Geo g, unsigned *bar) {
-    __shared__ unsigned s_acc[3];
+__global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b, Arr3 a, Geo g, unsigned long long *bar) {
+    __shared__ unsigned s_f3[3], s_r3[3];
     extern __shared__ uint32_t s_dyn[];
-    uint32_t *sF0 = s_dyn, *sF1 = s_dyn + SPT * BLOCK;
+    if (threadIdx.x < 3) { s_f3[threadIdx.x] = 0u; s_r3[threadIdx.x] = 0u; }
+    __syncthreads();
+    int phase = 0;
+    uint32_t *sF0 = s_dyn, *sF1 = s_dyn + REGMAX, *sM = s_dyn + 2 * REGMAX;
+    const bool resident = g.ntiles <= (int)gridDim.x;   // one tile per CTA: masks stay in smem for the sweep
     const Team tm{bar, (int)gridDim.x, (int)blockIdx.x};
+#define TEAM_SYNC() (void)tm.sync_or(0u, phase, s_f3, s_r3)
+#define TEAM_OR(f) tm.sync_or((f), phase, s_f3, s_r3)
     unsigned long long t_prev = 0, t_acc[6] = {0, 0, 0, 0, 0, 0};
     const bool timer = blockIdx.x == 0 && threadIdx.x == 0;
     if (timer) t_prev = gz2::gtimer();
@@ -206,9 +222,9 @@ __global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b,
         for_tile_groups<LP>(p, tb, [&](int cb, int ns) { gz3::w_init<LP, WIN>(p, a, b, cb, ns, flow, offset, presat); });
     }
     for (int c = ttid; c < p.P; c += tstride) b.IN[c] = 1u;   // every site starts dirty
-    tm.sync();
+    TEAM_SYNC();
     TICK(0);
-    int sweeps = 0, levels_total = 0, pulses = 0, rot = 0, parity = 0;
+    int sweeps = 0, levels_total = 0, pulses = 0, parity = 0;
     int converged = 1;
     bool err = false;
     const int bfs_min = p.bfs_cap > 0 ? p.bfs_cap : (1 << 30);
@@ -243,7 +259,7 @@ __global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b,
                 if (lane < CPW && c0 + lane < p.P) b.IN[c0 + lane] = 0u;
             }
         }
-        tm.sync();
+        TEAM_SYNC();
         TICK(1);
         // ---- global relabel: temporally blocked BFS ----
         int d = 0;
@@ -253,9 +269,9 @@ __global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b,
             unsigned flags = 0;
             FOR_TILES {
                 const TileBox tb(p, g, tile);
-                flags |= bfs_round<LP, WIN>(p, a, b, g, tb, Fin, Fout, Vin, Vout, d, sF0, sF1);
+                flags |= bfs_round<LP, WIN>(p, a, b, g, tb, Fin, Fout, Vin, Vout, d, sF0, sF1, sM, d == 0 || !resident);
             }
-            const unsigned gf = team_or(tm, flags, p.ctr + CTR_FLAG0, rot, s_acc);
+            const unsigned gf = TEAM_OR(flags);
             found |= (gf & 2u) != 0;
             uint32_t *t = Fin; Fin = Fout; Fout = t;
             t = Vin; Vin = Vout; Vout = t;
@@ -279,7 +295,7 @@ __global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b,
                 }
             }
         }
-        tm.sync();
+        TEAM_SYNC();
         for (int pulse = 0; pulse < p.K; ++pulse) {
             // Pulses are NOT tile-owned: active chains cluster spatially, so groups are
             // interleaved over every warp of the team (group g -> warp g mod W).  Lane i of
@@ -304,7 +320,7 @@ __global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b,
                     gz3::w_pulse<LP, WIN, false>(p, a, b, g2 * CPW, CPW, parity, flow, pushes, relabels, b.IN);
                 }
             }
-            tm.sync();
+            TEAM_SYNC();
             parity ^= 1;
             ++pulses;
         }
@@ -313,7 +329,7 @@ __global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b,
         {
             unsigned stop = 0;
             if (threadIdx.x == 0 && tm.rank == 0 && gz2_watchdog_expired(p)) stop = 1;
-            if (team_or(tm, stop, p.ctr + CTR_FLAG0, rot, s_acc)) {
+            if (TEAM_OR(stop)) {
                 if (threadIdx.x == 0 && tm.rank == 0) vctr[CTR_STATUS] = (unsigned long long)(-GZ_ERR_NOCONVERGE);
                 break;
             }
@@ -326,13 +342,13 @@ __global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b,
     for (int r = TileBox(p, g, tile).y0 + warp, y1_ = TileBox(p, g, tile).y1; r < y1_; r += nwarps) \
         for (int x = TileBox(p, g, tile).x0 + lane, x1_ = TileBox(p, g, tile).x1; x < x1_; x += 32)
     FOR_TILE_SITES gz3::w_reach_init<WIN>(p, b, r * p.G + x);
-    tm.sync();
+    TEAM_SYNC();
     int reach_passes = 0;
     int32_t *Rin = b.R0, *Rout = b.R1;
     for (;;) {
         unsigned ch = 0;
         FOR_TILE_SITES ch |= gz2::bit_reach_iter<WIN, 1>(p, b, r * p.G + x, Rin, Rout) ? 1u : 0u;
-        const bool any = team_or(tm, ch, p.ctr + CTR_FLAG0, rot, s_acc) != 0;
+        const bool any = TEAM_OR(ch) != 0;
         int32_t *t = Rin; Rin = Rout; Rout = t;
         ++reach_passes;
         if (!any) break;
@@ -346,12 +362,14 @@ __global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b,
         p.labels[c] = lo + Rin[c];
         stranded += __popc(b.EX[c]);
     }
-    tm.sync();
+    TEAM_SYNC();
     long long energy = 0;
     int viol = 0;
     FOR_TILE_SITES gz3::w_energy<LP>(p, a, r * p.G + x, energy, viol);
 #undef FOR_TILE_SITES
 #undef FOR_TILES
+#undef TEAM_SYNC
+#undef TEAM_OR
     TICK(5);
 #undef TICK
     if (timer)
