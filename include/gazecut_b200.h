@@ -68,7 +68,7 @@ typedef struct {
 #define GZ_SCHED_CAPPED 2
 #define GZ_SCHED_V1 4      /* force the v1 (column-relaxation) solver; debugging/comparison */
 #define GZ_SCHED_V2 8      /* force the v2 (bit-parallel, thread-per-chain) solver */
-#define GZ_SCHED_V3 16     /* force the v3 (warp-per-chain, whole-grid strided) solver */
+#define GZ_SCHED_V3 16     /* retired v3 solver; accepted and ignored (v4 runs) */
 
 /* maxflow.py:460-471 + 506-509 stats keys, plus device timings. */
 typedef struct {

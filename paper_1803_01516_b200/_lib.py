@@ -25,7 +25,7 @@ GZ_SCHED_NO_WAVE = 1
 GZ_SCHED_CAPPED = 2
 GZ_SCHED_V1 = 4
 GZ_SCHED_V2 = 8
-GZ_SCHED_V3 = 16
+GZ_SCHED_V3 = 16  # retired (maps to the default v4 solver)
 
 
 class Cuboid(C.Structure):

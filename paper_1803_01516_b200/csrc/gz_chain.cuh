@@ -1,0 +1,474 @@
+// gz_chain.cuh -- per-chain warp machinery of the v4 solver (gz_tilesolve.cuh).
+//
+// Node arrays are column-major, [site][LPT] with LPT = 16 (m <= 16) or 32*R
+// (R = 1, 2, 4 segments of 32 chain positions), so a warp segment of LP lanes
+// holds LP consecutive chain positions of one site and every per-node load is
+// coalesced.  Lane j of segment s <-> chain position t = s*LP + j + 1.
+//   vol[c][k]   data cost of label k              (k < m)
+//   cu [c][t-1] residual of chain arc t -> t+1     (arc 0 from the source is
+//               saturated at init and never stored)
+//   ph/pv/dar/dbr/dad/dbd [c][t-1]  lateral pair state at level t (gz_graph.cuh)
+//   e, h, ein0/ein1 [c][t-1]
+// Bit arrays (masks, excess, active, inbox, BFS frontier/visited) hold one
+// 32-bit word per (segment, site) at word index s*P + c; bit j <-> position
+// s*32 + j + 1 (LP = 16: one word per site, bits 0..15).
+//
+// A pulse is ONE team-synchronised phase per chain segment:
+//   merge last pulse's inbox -> upward chain wave (segmented min-plus scan:
+//   x_{t+1} = min(cu_t, e_t + x_t) over admissible chain arcs, the exact
+//   Gauss-Seidel result of pushing bottom-up) -> lateral and downward pushes
+//   of the remaining excess on admissible arcs -> relabel of nodes that could
+//   not push (in place).  A node pushes with its phase-start height and only
+//   relabels if it made no push, so two nodes can never push along one arc
+//   pair in opposite directions; lateral pushes land in the other inbox
+//   buffer (no reader this pulse).  The chain arc between two segments is
+//   treated like a lateral arc: the wave leaving the top of segment s and a
+//   downward push out of the bottom of segment s+1 travel through the inbox.
+#pragma once
+
+namespace gz3 {
+
+using namespace gz;
+using gz2::BW;
+using gz2::Bits2;
+
+struct Arr3 {
+    int32_t *vol, *cu, *ph, *pv, *dar, *dbr, *dad, *dbd, *e, *ein0, *ein1, *h;
+    uint32_t *IN0, *IN1;   // inbox bits per (segment, site) word, double-buffered
+};
+
+constexpr unsigned FULL = 0xffffffffu;
+
+template <int LP>
+__device__ __forceinline__ int from_above(int v) { return __shfl_down_sync(FULL, v, 1, LP); }   // lane j+1
+template <int LP>
+__device__ __forceinline__ int from_below(int v) { return __shfl_up_sync(FULL, v, 1, LP); }     // lane j-1
+
+// Per-lane context: node (t, c) plus neighbour sites.
+template <int LP, int R, bool WIN>
+struct Lane {
+    static constexpr int LPT = LP * R;
+    int c, s, j, t, lo, hi, y, g, I, wi;
+    bool valid, real;
+    int nc[4], nlo[4], nhi[4];
+    bool has[4];
+    // sites c_base .. c_base + nsites - 1 (nsites <= 32 / LP), segment seg
+    __device__ __forceinline__ void init(const Prob &p, int c_base, int nsites, int seg = 0) {
+        const int lane = threadIdx.x & 31;
+        c = c_base + lane / LP;
+        j = lane % LP;
+        s = seg;
+        t = s * LP + j + 1;
+        valid = lane / LP < nsites && c < p.P;
+        const int cc = valid ? c : 0;
+        y = cc / p.G;
+        g = cc - y * p.G;
+        has[0] = valid && g + 1 < p.G; nc[0] = cc + 1;
+        has[1] = valid && g > 0;       nc[1] = cc - 1;
+        has[2] = valid && y + 1 < p.Y; nc[2] = cc + p.G;
+        has[3] = valid && y > 0;       nc[3] = cc - p.G;
+        if (WIN) {
+            lo = valid ? p.lo[cc] : 0;
+            hi = valid ? p.hi[cc] : 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) { nlo[i] = has[i] ? p.lo[nc[i]] : 0; nhi[i] = has[i] ? p.hi[nc[i]] : 0; }
+        } else {
+            lo = 0; hi = p.L;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) { nlo[i] = 0; nhi[i] = p.L; }
+        }
+        real = valid && t > lo && t <= hi;
+        I = cc * LPT + t - 1;
+        wi = s * p.P + cc;
+    }
+    __device__ __forceinline__ int kown(int tt) const { return tt <= lo ? K_SRC : (tt > hi ? K_SNK : K_REAL); }
+    __device__ __forceinline__ int knb(int i, int tt) const { return tt <= nlo[i] ? K_SRC : (tt > nhi[i] ? K_SNK : K_REAL); }
+    __device__ __forceinline__ int nidx(int i) const { return nc[i] * LPT + t - 1; }
+    // segment boundary lanes whose t+1 / t-1 neighbour lives in another segment
+    __device__ __forceinline__ bool top_edge() const { return R > 1 && j == LP - 1 && s + 1 < R && valid; }
+    __device__ __forceinline__ bool bot_edge() const { return R > 1 && j == 0 && s > 0 && valid; }
+};
+
+// value at position t+1 / t-1 of the same array: shuffle inside the segment,
+// load across a segment boundary (every lane executes the shuffle)
+template <int LP, int R, bool WIN>
+__device__ __forceinline__ int up_of(const Lane<LP, R, WIN> &L, int v, const int32_t *arr, int idx, bool ok = true) {
+    int r = from_above<LP>(v);
+    if (ok && L.top_edge()) r = arr[idx + 1];
+    return r;
+}
+template <int LP, int R, bool WIN>
+__device__ __forceinline__ int dn_of(const Lane<LP, R, WIN> &L, int v, const int32_t *arr, int idx) {
+    int r = from_below<LP>(v);
+    if (L.bot_edge()) r = arr[idx - 1];
+    return r;
+}
+
+// Residuals of the 14 arcs of a lane's node, target heights and kinds.
+// All shuffles are executed by every lane (uniform control flow).
+template <int LP, int R, bool WIN>
+struct Arcs {
+    int r[A_COUNT], hv[A_COUNT], kd[A_COUNT];
+    // raw words (for write-back)
+    int w_cu, w_ph, w_pv, w_dar, w_dbr, w_dad, w_dbd;   // own-stored at I
+    int w_phL, w_pvU, w_darL, w_dbrL, w_dadU, w_dbdU;   // neighbour-stored at the same position
+    int w_dbr_up, w_darL_up, w_dbd_up, w_dadU_up;       // same arrays at position t+1
+    int h_u;
+
+    __device__ __forceinline__ void load(const Prob &p, const Arr3 &a, const Lane<LP, R, WIN> &L) {
+        const int I = L.I;
+        const bool v = L.valid;
+        w_cu = v ? a.cu[I] : 0;
+        w_ph = v ? a.ph[I] : 0;
+        w_pv = v ? a.pv[I] : 0;
+        w_dar = v ? a.dar[I] : 0;
+        w_dbr = v ? a.dbr[I] : 0;
+        w_dad = v ? a.dad[I] : 0;
+        w_dbd = v ? a.dbd[I] : 0;
+        const int iL = L.nidx(1), iU = L.nidx(3);
+        w_phL = L.has[1] ? a.ph[iL] : 0;
+        w_darL = L.has[1] ? a.dar[iL] : 0;
+        w_dbrL = L.has[1] ? a.dbr[iL] : 0;
+        w_pvU = L.has[3] ? a.pv[iU] : 0;
+        w_dadU = L.has[3] ? a.dad[iU] : 0;
+        w_dbdU = L.has[3] ? a.dbd[iU] : 0;
+        int hn[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) hn[i] = L.has[i] ? a.h[L.nidx(i)] : HINF;
+        h_u = v ? a.h[I] : HINF;
+        // position t+1 / t-1 values
+        w_dbr_up = up_of(L, w_dbr, a.dbr, I);
+        w_darL_up = up_of(L, w_darL, a.dar, iL, L.has[1]);
+        w_dbd_up = up_of(L, w_dbd, a.dbd, I);
+        w_dadU_up = up_of(L, w_dadU, a.dad, iU, L.has[3]);
+        const int h_above = up_of(L, h_u, a.h, I), h_below = dn_of(L, h_u, a.h, I);
+        int hn_above[4], hn_below[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int ni = L.has[i] ? L.nidx(i) : 0;
+            hn_above[i] = from_above<LP>(hn[i]);
+            hn_below[i] = from_below<LP>(hn[i]);
+            if (L.top_edge() && L.has[i]) hn_above[i] = a.h[ni + 1];
+            if (L.bot_edge() && L.has[i]) hn_below[i] = a.h[ni - 1];
+        }
+
+        const int t = L.t, P2 = 2 * p.pen, cap = p.hard ? p.hcap : p.inh;
+        const bool top_ok = t < p.L;   // a position t+1 <= L exists (diagonals up)
+#define SETA(J, RR, KIND, HV) do { kd[J] = (KIND); r[J] = (KIND) == K_SRC ? 0 : (RR); hv[J] = (KIND) == K_SNK ? 0 : (HV); } while (0)
+        SETA(A_UP, w_cu, L.kown(t + 1), h_above);
+        SETA(A_DN, HINF, L.kown(t - 1), h_below);
+        SETA(A_SR, L.has[0] ? w_ph : 0, L.has[0] ? L.knb(0, t) : K_SRC, hn[0]);
+        SETA(A_SL, L.has[1] ? P2 - w_phL : 0, L.has[1] ? L.knb(1, t) : K_SRC, hn[1]);
+        SETA(A_SD, L.has[2] ? w_pv : 0, L.has[2] ? L.knb(2, t) : K_SRC, hn[2]);
+        SETA(A_SU, L.has[3] ? P2 - w_pvU : 0, L.has[3] ? L.knb(3, t) : K_SRC, hn[3]);
+        SETA(A_UR, (L.has[0] && top_ok) ? w_dbr_up : 0, (L.has[0] && top_ok) ? L.knb(0, t + 1) : K_SRC, hn_above[0]);
+        SETA(A_UL, (L.has[1] && top_ok) ? w_darL_up : 0, (L.has[1] && top_ok) ? L.knb(1, t + 1) : K_SRC, hn_above[1]);
+        SETA(A_UD, (L.has[2] && top_ok) ? w_dbd_up : 0, (L.has[2] && top_ok) ? L.knb(2, t + 1) : K_SRC, hn_above[2]);
+        SETA(A_UU, (L.has[3] && top_ok) ? w_dadU_up : 0, (L.has[3] && top_ok) ? L.knb(3, t + 1) : K_SRC, hn_above[3]);
+        SETA(A_DR, L.has[0] ? cap - w_dar : 0, L.has[0] ? L.knb(0, t - 1) : K_SRC, hn_below[0]);
+        SETA(A_DL, L.has[1] ? cap - w_dbrL : 0, L.has[1] ? L.knb(1, t - 1) : K_SRC, hn_below[1]);
+        SETA(A_DD, L.has[2] ? cap - w_dad : 0, L.has[2] ? L.knb(2, t - 1) : K_SRC, hn_below[2]);
+        SETA(A_DU, L.has[3] ? cap - w_dbdU : 0, L.has[3] ? L.knb(3, t - 1) : K_SRC, hn_below[3]);
+#undef SETA
+    }
+};
+
+// site and position of a lateral arc's target
+template <int LP, int R, bool WIN>
+__device__ __forceinline__ void lateral_target(const Lane<LP, R, WIN> &L, int jarc, int &site, int &pos) {
+    const int i = (jarc - A_SR) & 3;
+    site = L.nc[i];
+    pos = jarc <= A_SU ? L.t : (jarc <= A_UU ? L.t + 1 : L.t - 1);
+}
+
+// inclusive scan of f_j(x) = min(A_j, B_j + x) over the segment; returns F_j(x0)
+template <int LP>
+__device__ __forceinline__ int chain_wave(int A, int B, int j, int x0 = 0) {
+#pragma unroll
+    for (int o = 1; o < LP; o <<= 1) {
+        const int A2 = __shfl_up_sync(FULL, A, o, LP), B2 = __shfl_up_sync(FULL, B, o, LP);
+        if (j >= o) {   // compose: f_this o f_below
+            A = min(A, B + A2);
+            B = B + B2;
+        }
+    }
+    return min(A, B + x0);
+}
+
+template <int LP>
+__device__ __forceinline__ uint32_t seg_ballot(bool pred) {
+    const uint32_t b = __ballot_sync(FULL, pred);
+    if (LP == 32) return b;
+    return (b >> ((threadIdx.x & 31) & ~(LP - 1))) & (LP >= 32 ? 0xffffffffu : ((1u << (LP & 31)) - 1u));
+}
+
+// ---------------------------------------------------------------------------
+// init of one warp group (LP = 16: two sites; LP = 32: one site, all R
+// segments in order): residuals from the volume, source saturation, greedy
+// upward chain wave (carried across segments), constant offset.
+template <int LP, int R, bool WIN>
+__device__ void w_init(const Prob &p, const Arr3 &a, int c_base, int nsites, long long &flow, long long &offset,
+                       long long &presat) {
+    int carry = 0;   // wave flow entering the bottom of the next segment
+#pragma unroll 1
+    for (int s = 0; s < R; ++s) {
+        Lane<LP, R, WIN> L;
+        L.init(p, c_base, nsites, s);
+        const int I = L.I;
+        const int volj = (L.valid && L.t - 1 < p.M) ? a.vol[I] : 0;
+        const int vol_above = up_of(L, volj, a.vol, I);
+        if (L.valid) {
+            a.cu[I] = (L.t < p.M) ? vol_above : 0;
+            a.ph[I] = p.pen; a.pv[I] = p.pen;
+            a.dar[I] = 0; a.dbr[I] = 0; a.dad[I] = 0; a.dbd[I] = 0;
+            a.ein0[I] = 0; a.ein1[I] = 0;
+            a.h[I] = HINF;
+        }
+        long long e = 0;
+        // chain arc lo: source -> position lo+1 carries vol[lo]
+        const int vol_lo_src = L.valid ? a.vol[L.c * Lane<LP, R, WIN>::LPT + L.lo] : 0;
+        if (L.real && L.t == L.lo + 1) e += vol_lo_src;
+        if (WIN && L.valid) {
+            const long long icap_off = p.hard ? UNCUTTABLE : (long long)p.inh;
+            const int icap = p.hard ? p.hcap : p.inh;
+            if (L.t == 1 && L.lo == L.hi) offset += vol_lo_src;
+            if (L.t <= p.L) {
+                const int t = L.t;
+                for (int i = 0; i < 4; i += 2) {   // forward neighbours right (0), down (2)
+                    if (!L.has[i]) continue;
+                    const int ka = L.kown(t), kb = L.knb(i, t);
+                    if ((ka == K_SRC && kb == K_SNK) || (ka == K_SNK && kb == K_SRC)) offset += p.pen;
+                    if (L.kown(t) == K_SRC && L.knb(i, t - 1) == K_SNK) offset += icap_off;
+                    if (L.knb(i, t) == K_SRC && L.kown(t - 1) == K_SNK) offset += icap_off;
+                }
+            }
+            if (L.real) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    if (!L.has[i]) continue;
+                    if (L.knb(i, L.t) == K_SRC) e += p.pen;
+                    if (L.t + 1 <= p.L && L.knb(i, L.t + 1) == K_SRC) e += icap;
+                }
+            }
+        }
+        // greedy upward wave (no heights yet): every chain arc out of a real node is usable
+        int ex = (int)e;
+        if (!p.no_wave) {
+            const bool up_ok = L.real;
+            const int cuw = (L.valid && L.t < p.M) ? vol_above : 0;
+            const int cin = (L.j == 0 && L.real) ? carry : 0;   // carry enters at the segment's first lane
+            const int x_out = chain_wave<LP>(up_ok ? cuw : 0, up_ok ? ex + cin : 0, L.j);
+            const int x_below = from_below<LP>(x_out);
+            const int x_in = L.j > 0 ? x_below : cin;
+            if (L.real) {
+                ex = ex + x_in - x_out;
+                a.cu[I] = cuw - x_out;
+                if (L.kown(L.t + 1) == K_SNK) { flow += x_out; presat += x_out; }
+            }
+            carry = __shfl_sync(FULL, (L.real && L.kown(L.t + 1) == K_REAL) ? x_out : 0, LP - 1, LP);
+        }
+        if (L.valid) a.e[I] = L.real ? ex : 0;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// mask build of one (segment, site) group: pending inbox merge, 13 arc-mask
+// words, excess word, BFS reset words.
+template <int LP, int R, bool WIN>
+__device__ void w_build(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base, int nsites, int seg) {
+    Lane<LP, R, WIN> L;
+    L.init(p, c_base, nsites, seg);
+    const int I = L.I, P = p.P;
+    // every global load of the group is issued before the first store (one
+    // round trip): inbox words and values, excess, then the arc state
+    const uint32_t in0 = L.valid ? a.IN0[L.wi] : 0u, in1 = L.valid ? a.IN1[L.wi] : 0u;
+    int e = L.valid ? a.e[I] : 0;
+    const int x0 = L.valid ? a.ein0[I] : 0, x1 = L.valid ? a.ein1[I] : 0;
+    Arcs<LP, R, WIN> A;
+    A.load(p, a, L);
+    // merge both inbox buffers (the last pulse's lateral pushes)
+    if ((in0 >> L.j) & 1u) { e += x0; a.ein0[I] = 0; }
+    if ((in1 >> L.j) & 1u) { e += x1; a.ein1[I] = 0; }
+    if (L.valid && ((in0 | in1) >> L.j) & 1u) a.e[I] = e;
+    uint32_t m[13];
+#pragma unroll
+    for (int q = 0; q < 13; ++q) m[q] = seg_ballot<LP>(L.real && A.r[q] > 0);
+    const uint32_t ex = seg_ballot<LP>(L.real && e > 0);
+    if (L.valid && L.j == 0) {
+#pragma unroll
+        for (int q = 0; q < 13; ++q) b.mask[((size_t)q * R + L.s) * P + L.c] = m[q];
+        b.EX[L.wi] = ex;
+        b.V[L.wi] = 0u;
+        b.A[L.wi] = 0u;
+        a.IN0[L.wi] = 0u;
+        a.IN1[L.wi] = 0u;
+        b.F0[L.wi] = BW<R>::range(L.hi, p.M).w[L.s];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// one pulse on a warp group of chains
+template <int LP, int R, bool WIN>
+__device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base, int nsites, int seg, int parity,
+                        long long &flow, long long &pushes, long long &relabels, uint32_t *dirty) {
+    Lane<LP, R, WIN> L;
+    L.init(p, c_base, nsites, seg);
+    const int I = L.I, P = p.P;
+    constexpr int LPT = Lane<LP, R, WIN>::LPT;
+    uint32_t *IN_prev = parity ? a.IN0 : a.IN1;
+    uint32_t *IN_cur = parity ? a.IN1 : a.IN0;
+    int32_t *ein_prev = parity ? a.ein0 : a.ein1;
+    int32_t *ein_cur = parity ? a.ein1 : a.ein0;
+    // all loads before the first store: one round trip per group (ein_prev has
+    // no writer during this pulse, so reading it unconditionally is safe)
+    const uint32_t inb = L.valid ? IN_prev[L.wi] : 0u;
+    int e = L.valid ? a.e[I] : 0;
+    const int xin = L.valid ? ein_prev[I] : 0;
+    Arcs<LP, R, WIN> A;
+    A.load(p, a, L);
+    if ((inb >> L.j) & 1u) { e += xin; ein_prev[I] = 0; }
+    if (L.valid && L.j == 0 && inb) IN_prev[L.wi] = 0u;
+    const int hu = A.h_u;
+    const bool live = L.real && hu < HINF;
+    // upward chain wave through admissible chain arcs
+    const bool adm_up = live && A.r[A_UP] > 0 && A.kd[A_UP] != K_SRC && hu == A.hv[A_UP] + 1;
+    const int x_out = chain_wave<LP>(adm_up ? A.r[A_UP] : 0, adm_up ? max(e, 0) : 0, L.j);
+    const int x_below = from_below<LP>(x_out);   // every lane shuffles (full mask)
+    const int x_in = L.j > 0 ? x_below : 0;
+    int cu_new = A.w_cu;
+    bool pushed = false;
+    if (L.real) {
+        e += x_in - x_out;
+        if (x_out > 0) {
+            cu_new -= x_out;
+            pushed = true;
+            ++pushes;
+            if (A.kd[A_UP] == K_SNK) {
+                flow += x_out;
+            } else if (L.top_edge()) {   // into the next segment's first node
+                atomicAdd(&ein_cur[I + 1], x_out);
+                atomicOr(&IN_cur[L.wi + P], 1u);
+            }
+        }
+    }
+    // lateral and downward pushes of the remaining excess
+    int dn = 0;
+    int ph_d = 0, pv_d = 0, dar_d = 0, dad_d = 0;
+    int phL_d = 0, pvU_d = 0, dbrL_d = 0, dbdU_d = 0, dbr_up_d = 0, darL_up_d = 0, dbd_up_d = 0, dadU_up_d = 0;
+    if (live && e > 0) {
+#pragma unroll
+        for (int jj = A_SR; jj <= A_DN; ++jj) {
+            if (e <= 0) break;
+            if (A.kd[jj] == K_SRC || A.r[jj] <= 0 || hu != A.hv[jj] + 1) continue;
+            const int d = min(e, A.r[jj]);
+            e -= d;
+            pushed = true;
+            ++pushes;
+            switch (jj) {
+            case A_SR: ph_d -= d; break;
+            case A_SL: phL_d += d; break;
+            case A_SD: pv_d -= d; break;
+            case A_SU: pvU_d += d; break;
+            case A_UR: dbr_up_d -= d; break;
+            case A_UL: darL_up_d -= d; break;
+            case A_UD: dbd_up_d -= d; break;
+            case A_UU: dadU_up_d -= d; break;
+            case A_DR: dar_d += d; break;
+            case A_DL: dbrL_d += d; break;
+            case A_DD: dad_d += d; break;
+            case A_DU: dbdU_d += d; break;
+            case A_DN: dn += d; break;
+            }
+            if (jj == A_DN) continue;
+            if (A.kd[jj] == K_SNK) { flow += d; continue; }
+            int site, pos;
+            lateral_target<LP, R, WIN>(L, jj, site, pos);
+            atomicAdd(&ein_cur[site * LPT + pos - 1], d);
+            atomicOr(&IN_cur[((pos - 1) / LP) * P + site], 1u << ((pos - 1) % LP));
+        }
+    }
+    // chain-down pushes arrive at lane j-1 (adds to its excess and to its chain-up
+    // residual); out of a segment's first lane they cross into the segment below
+    const int dn_recv = from_above<LP>(dn);
+    const int dn_in = (L.real && L.j + 1 < LP) ? dn_recv : 0;
+    if (L.real) {
+        e += dn_in;
+        cu_new += dn_in;
+    }
+    if (dn > 0 && L.bot_edge()) {
+        atomicAdd(&a.cu[I - 1], dn);
+        atomicAdd(&ein_cur[I - 1], dn);
+        atomicOr(&IN_cur[L.wi - P], 1u << (LP - 1));
+    }
+    // relabel a live node that could not push
+    int hnew = hu;
+    if (live && !pushed && e > 0) {
+        int best = HINF;
+#pragma unroll
+        for (int jj = 0; jj < A_COUNT; ++jj)
+            if (A.kd[jj] != K_SRC && A.r[jj] > 0) best = min(best, A.hv[jj] + 1);
+        hnew = best;
+        ++relabels;
+    }
+    // write back
+    if (L.real) {
+        a.e[I] = e;
+        if (cu_new != A.w_cu) a.cu[I] = cu_new;
+        if (hnew != hu) a.h[I] = hnew;
+        if (ph_d) a.ph[I] = A.w_ph + ph_d;
+        if (pv_d) a.pv[I] = A.w_pv + pv_d;
+        if (dar_d) a.dar[I] = A.w_dar + dar_d;
+        if (dad_d) a.dad[I] = A.w_dad + dad_d;
+        if (phL_d) a.ph[L.nidx(1)] = A.w_phL + phL_d;
+        if (dbrL_d) a.dbr[L.nidx(1)] = A.w_dbrL + dbrL_d;
+        if (pvU_d) a.pv[L.nidx(3)] = A.w_pvU + pvU_d;
+        if (dbdU_d) a.dbd[L.nidx(3)] = A.w_dbdU + dbdU_d;
+        if (dbr_up_d) a.dbr[I + 1] = A.w_dbr_up + dbr_up_d;
+        if (dbd_up_d) a.dbd[I + 1] = A.w_dbd_up + dbd_up_d;
+        if (darL_up_d) a.dar[L.nidx(1) + 1] = A.w_darL_up + darL_up_d;
+        if (dadU_up_d) a.dad[L.nidx(3) + 1] = A.w_dadU_up + dadU_up_d;
+    }
+    const uint32_t newA = seg_ballot<LP>(L.real && e > 0 && hnew < HINF);
+    if (L.valid && L.j == 0) b.A[L.wi] = newA;
+    // a push changes this site's residuals and the pair state / excess of its
+    // neighbours: all their segments need their arc masks rebuilt next sweep
+    const uint32_t pm = seg_ballot<LP>(pushed);
+    if (pm && L.valid && L.j == 0) {
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            dirty[q * P + L.c] = 1u;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (L.has[i]) dirty[q * P + L.nc[i]] = 1u;
+        }
+    }
+}
+
+// extraction seeds: highest position holding excess (last mask build's words)
+template <int R, bool WIN>
+__device__ void w_reach_init(const Prob &p, const Bits2 &b, int c) {
+    int lo = 0, hi = p.L;
+    if (WIN) { lo = p.lo[c]; hi = p.hi[c]; }
+    BW<R> ex;
+    ex.load(b.EX, p.P, c);
+    const int top = ex.top();
+    const int r = top >= 0 ? top + 1 - lo : 0;
+    b.R0[c] = gz2::bit_close_up<WIN, R>(b, p.P, c, lo, hi, r);
+}
+
+template <int LPT>
+__device__ void w_energy(const Prob &p, const Arr3 &a, int c, long long &energy, int &viol) {
+    const int y = c / p.G, g = c - y * p.G;
+    const int lab = p.labels[c];
+    energy += a.vol[c * LPT + lab];
+    for (int i = 0; i < 2; ++i) {
+        const bool has = i == 0 ? g + 1 < p.G : y + 1 < p.Y;
+        if (!has) continue;
+        const int o = p.labels[i == 0 ? c + 1 : c + p.G];
+        const int dl = lab > o ? lab - o : o - lab;
+        if (p.hard && dl > 1) viol = 1;
+        energy += (long long)p.pen * dl + (long long)p.inh * (dl > 1 ? dl - 1 : 0);
+    }
+}
+
+}  // namespace gz3

@@ -61,6 +61,7 @@ struct Prob {
     int capped;
     unsigned long long watchdog_ns, t_start_ns;   // 0 = no watchdog; start stamped on device
     volatile unsigned *progress;                  // debug: per-block phase counter (mapped host memory) or null
+    int trace;                                    // debug: per-sweep device printf (env GZ_TRACE)
     int no_wave;         // skip the initial chain wave
     const int32_t *lo, *hi;   // windowed only
     int32_t *vol, *cu, *ph, *pv, *dar, *dbr, *dad, *dbd;

@@ -601,7 +601,7 @@ __global__ void __launch_bounds__(256) gz_solve_kernel(Prob p) {
 }  // namespace
 
 #include "gz_bitsolve.cuh"
-#include "gz_warpsolve.cuh"
+#include "gz_chain.cuh"
 #include "gz_tilesolve.cuh"
 
 namespace {
@@ -610,9 +610,9 @@ namespace {
 // data term (energy.py:83-114, geometry.py:325-335): one thread per site,
 // labels looped; output planar [k][y][g] (solver layout) or (y, g, k).
 // LAYOUT 0: (y, g, k) reference order; 1: planar [k][site]; 2: column-major [site][LP]
-template <int LAYOUT, int LP = 16>
+template <int LAYOUT>
 __global__ void k_sad(const uint8_t *__restrict__ left, const uint8_t *__restrict__ right, int img_w, int ch,
-                      gz_cuboid cb, int32_t *__restrict__ vol) {
+                      gz_cuboid cb, int32_t *__restrict__ vol, int LP = 16) {
     const int P = cb.y_extent * cb.g_extent;
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= P) return;
@@ -636,8 +636,7 @@ __global__ void k_sad(const uint8_t *__restrict__ left, const uint8_t *__restric
 }
 
 // (rows, cols, m) -> column-major [site][LP], zero padded
-template <int LP>
-__global__ void k_to_colmajor(const int32_t *__restrict__ src, int P, int M, int32_t *__restrict__ dst) {
+__global__ void k_to_colmajor(const int32_t *__restrict__ src, int P, int M, int LP, int32_t *__restrict__ dst) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= (long long)P * LP) return;
     const int c = (int)(i / LP), k = (int)(i % LP);
@@ -770,8 +769,8 @@ size_t bit_bytes(int rows, int cols, int m) {
     return align_up((size_t)(13 + 9) * NW * P * 4) + 2 * align_up(P * 4);
 }
 
-// lanes per chain segment of the v3 solver (0: m too large for it)
-int lanes_for(int m) { return m <= 16 ? 16 : (m <= 32 ? 32 : 0); }
+// positions per site row of the v4 solver's node arrays (16, or 32 x segments; 0: m too large)
+int lanes_for(int m) { return m <= 16 ? 16 : (m <= 128 ? 32 * words_for(m) : 0); }
 
 size_t ws_bytes(int rows, int cols, int m) {
     const int mp = m > lanes_for(m) ? m : lanes_for(m);
@@ -825,32 +824,33 @@ int coop_grid(const void *kernel, int threads, int *grid_out, size_t dyn_smem = 
     return GZ_OK;
 }
 
-// 1: v1 column relaxation, 2: bit-parallel (any m <= 256, deterministic
-// relabel when capped), 3: warp-per-chain (m <= 32), 4: tile-owned
-// warp-per-chain with temporally blocked BFS (m <= 32, exact / uncapped; default)
+// 1: v1 column relaxation (m > 256), 2: bit-parallel thread-per-chain
+// (deterministic relabel; the capped level-2 schedule), 4: tile-owned
+// warp-per-chain-segment solver with temporally blocked BFS (m <= 128, exact /
+// uncapped; the default).
 int choose_solver(int m, const gz_sched *sc) {
     const int flags = sc ? sc->flags : 0;
     if ((flags & GZ_SCHED_V1) || words_for(m) == 0) return 1;
     if ((flags & GZ_SCHED_V2) || (flags & GZ_SCHED_CAPPED) || lanes_for(m) == 0) return 2;
-    if (flags & GZ_SCHED_V3) return 3;
     return 4;
 }
 
 // Tile geometry of the v4 solver for a team of nb CTAs.
-gz4::Geo tile_geo(int rows, int cols, int nb) {
+gz4::Geo tile_geo(int rows, int cols, int nb, int nw) {
+    const int regmax = gz4::region_sites(nw);
     gz4::Geo g;
     const char *hs = getenv("GZ_BFS_H");
     g.H = hs ? atoi(hs) : 8;
     g.TX = 32;
     // the smallest region (one tile row plus halo) must fit the BFS register tiles
-    while (g.H > 1 && (1 + 2 * g.H) * (g.TX + 2 * g.H) > gz4::REGMAX) --g.H;
+    while (g.H > 1 && (1 + 2 * g.H) * (g.TX + 2 * g.H) > regmax) --g.H;
     if (g.H < 1) g.H = 1;
     g.nx = (cols + g.TX - 1) / g.TX;
     int tile_rows = nb / g.nx;
     if (tile_rows < 1) tile_rows = 1;
     g.TY = (rows + tile_rows - 1) / tile_rows;
     const int rw = cols < g.TX + 2 * g.H ? cols : g.TX + 2 * g.H;
-    while (g.TY > 1 && (rows < g.TY + 2 * g.H ? rows : g.TY + 2 * g.H) * rw > gz4::REGMAX) --g.TY;
+    while (g.TY > 1 && (rows < g.TY + 2 * g.H ? rows : g.TY + 2 * g.H) * rw > regmax) --g.TY;
     g.ny = (rows + g.TY - 1) / g.TY;
     g.ntiles = g.nx * g.ny;
     return g;
@@ -874,6 +874,7 @@ int solve_planar(const Workspace &w, int rows, int cols, int m, const gz_energy 
         const char *wd = getenv("GZ_WATCHDOG_MS");
         p.watchdog_ns = (unsigned long long)(wd ? atof(wd) : 20000.0) * 1000000ull;
     }
+    p.trace = getenv("GZ_TRACE") ? 1 : 0;
     p.lo = lo; p.hi = hi;
     p.vol = w.vol; p.cu = w.cu; p.ph = w.ph; p.pv = w.pv; p.dar = w.dar; p.dbr = w.dbr; p.dad = w.dad; p.dbd = w.dbd;
     p.e = w.e; p.ein = w.ein; p.h = w.h; p.h2 = w.h2; p.reach = w.reach; p.reach2 = w.reach2; p.labels = w.labels;
@@ -888,18 +889,20 @@ int solve_planar(const Workspace &w, int rows, int cols, int m, const gz_energy 
     const bool det = p.capped != 0;
     const int which = choose_solver(m, sc);
     const bool v1 = which == 1;
-    if (!v1 && p.bfs_cap == 0) p.bfs_cap = which == 4 ? 48 : 64;   // default: BFS depth before it may stop at excess
+    // default BFS depth before a global relabel may stop at the first excess, and
+    // (exact v4 solves) pulses per sweep: both scale with the chain length m
+    // (measured: C1 m=16 best at 48 / 12, C2 m=60 at 128 / 48; tools/sweep_cfg.py)
+    if (!v1 && p.bfs_cap == 0) p.bfs_cap = which == 4 ? (2 * m + 16 > 48 ? 2 * m + 16 : 48) : 64;
+    if (which == 4 && !p.capped && m - 12 > p.K) p.K = m - 12;
     if (!v1 && p.bfs_cap < 0) p.bfs_cap = 0;            // exhaustive BFS every sweep
     const void *kern = nullptr;
 #define GZ_PICK(W_, NW_, D_) if (win == W_ && NW == NW_ && det == D_) kern = (const void *)gz2::gz_bitsolve_kernel<W_, NW_, D_>;
 #define GZ_PICK_NW(NW_) GZ_PICK(false, NW_, false) GZ_PICK(false, NW_, true) GZ_PICK(true, NW_, false) GZ_PICK(true, NW_, true)
     const int LPn = lanes_for(m);
     if (which == 4) {
-        if (LPn == 16) kern = win ? (const void *)gz4::gz_tilesolve_kernel<16, true> : (const void *)gz4::gz_tilesolve_kernel<16, false>;
-        else kern = win ? (const void *)gz4::gz_tilesolve_kernel<32, true> : (const void *)gz4::gz_tilesolve_kernel<32, false>;
-    } else if (which == 3) {
-        if (LPn == 16) kern = win ? (const void *)gz3::gz_warpsolve_kernel<16, true> : (const void *)gz3::gz_warpsolve_kernel<16, false>;
-        else kern = win ? (const void *)gz3::gz_warpsolve_kernel<32, true> : (const void *)gz3::gz_warpsolve_kernel<32, false>;
+#define GZ_PICK4(LP_, R_) if (LPn == LP_ * R_) kern = win ? (const void *)gz4::gz_tilesolve_kernel<LP_, R_, true> : (const void *)gz4::gz_tilesolve_kernel<LP_, R_, false>;
+        GZ_PICK4(16, 1) GZ_PICK4(32, 1) GZ_PICK4(32, 2) GZ_PICK4(32, 4)
+#undef GZ_PICK4
     } else if (which == 2) {
         GZ_PICK_NW(1) GZ_PICK_NW(2) GZ_PICK_NW(4) GZ_PICK_NW(8)
     } else {
@@ -918,14 +921,7 @@ int solve_planar(const Workspace &w, int rows, int cols, int m, const gz_energy 
     if (grid > need) grid = need < 1 ? 1 : need;
     gz4::Geo geo{};
     unsigned long long *bar = w.ctr + gz::CTR_BAR0;
-    if (which == 4) geo = tile_geo(rows, cols, grid);
-    if (which == 3) {
-        int dev = 0, sms = 0, occ = 0;
-        CK(cudaGetDevice(&dev));
-        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0));
-        grid = sms * occ;   // warp groups are grid-strided: use every resident slot
-    }
+    if (which == 4) geo = tile_geo(rows, cols, grid, words_for(m));
     if (getenv("GZ_DEBUG_PROGRESS")) {
         static unsigned *prog = nullptr;
         if (!prog) CK(cudaHostAlloc((void **)&prog, 65536 * sizeof(unsigned), cudaHostAllocMapped));
@@ -938,14 +934,13 @@ int solve_planar(const Workspace &w, int rows, int cols, int m, const gz_energy 
     gz3::Arr3 a3{w.vol, w.cu, w.ph, w.pv, w.dar, w.dbr, w.dad, w.dbd, w.e, w.ein, w.h2, w.h, w.IN0, w.IN1};
     void *args1[] = {&p};
     void *args2[] = {&p, &bb};
-    void *args3[] = {&p, &bb, &a3};
     void *args4[] = {&p, &bb, &a3, &geo, &bar};
     if (which == 4) {
         if (geo.ntiles < grid) grid = geo.ntiles;   // every CTA owns at least one tile
-        geo = tile_geo(rows, cols, grid);
+        geo = tile_geo(rows, cols, grid, words_for(m));
         CK(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(threads), args4, dyn_smem, s));
     } else {
-        CK(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(256), which == 1 ? args1 : (which == 2 ? args2 : args3), 0, s));
+        CK(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(256), which == 1 ? args1 : args2, 0, s));
     }
     CK(cudaEventRecord(e1, s));
     if (p.progress) {   // debug: poll instead of blocking, report where blocks stall
@@ -1036,10 +1031,10 @@ int gz_solve_volume(const int32_t *vol, int32_t rows, int32_t cols, int32_t m, c
     cudaStream_t s = (cudaStream_t)stream;
     Workspace w = carve(workspace, rows, cols, m);
     const int P = rows * cols;
-    if (choose_solver(m, sched) >= 3) {
-        const long long n = (long long)P * lanes_for(m);
-        if (lanes_for(m) == 16) k_to_colmajor<16><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(vol, P, m, w.vol);
-        else k_to_colmajor<32><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(vol, P, m, w.vol);
+    if (choose_solver(m, sched) == 4) {
+        const int lp = lanes_for(m);
+        const long long n = (long long)P * lp;
+        k_to_colmajor<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(vol, P, m, lp, w.vol);
     } else {
         k_to_planar<<<(P + 255) / 256, 256, 0, s>>>(vol, P, m, w.vol);
     }
@@ -1099,10 +1094,9 @@ int gz_solve_pairs(const uint8_t *left, const uint8_t *right, int32_t batch, int
     const size_t img = (size_t)img_h * img_w * channels;
     for (int b = 0; b < batch; ++b) {
         const int which = choose_solver(m, sched);
-        if (which >= 3 && lanes_for(m) == 16)
-            k_sad<2, 16><<<(P + 127) / 128, 128, 0, s>>>(left + b * img, right + b * img, img_w, channels, *cb, w.vol);
-        else if (which >= 3)
-            k_sad<2, 32><<<(P + 127) / 128, 128, 0, s>>>(left + b * img, right + b * img, img_w, channels, *cb, w.vol);
+        if (which == 4)
+            k_sad<2><<<(P + 127) / 128, 128, 0, s>>>(left + b * img, right + b * img, img_w, channels, *cb, w.vol,
+                                                     lanes_for(m));
         else
             k_sad<1><<<(P + 127) / 128, 128, 0, s>>>(left + b * img, right + b * img, img_w, channels, *cb, w.vol);
         CK(cudaGetLastError());

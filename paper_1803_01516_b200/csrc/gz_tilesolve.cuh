@@ -16,7 +16,9 @@
 //    site groups are interleaved over all warps of the team, and each warp
 //    checks its groups' active/inbox words with one load per lane + a ballot,
 //    visiting only the chains that have work.
-//  * extraction (maxflow.py:267-320): prefix-closure rounds as v2/v3.
+//  * extraction (maxflow.py:267-320): prefix-closure rounds (gz_bitsolve.cuh).
+//  * chains longer than 32 positions are split into R segments of 32 lanes
+//    (gz_chain.cuh); bit words and the BFS are NW = R words per site.
 //
 // The team barrier is a generation-flip counter (one CTA per team adds
 // 2^31 - (nb-1), the others 1), so several teams can share a launch.
@@ -28,12 +30,14 @@ using namespace gz;
 using gz2::Bits2;
 using gz2::BW;
 using gz3::Arr3;
+using gz3::FULL;
 
-constexpr unsigned FULL = 0xffffffffu;
 constexpr int BLOCK = 512;   // threads per CTA (one CTA per SM)
-constexpr int SPT = 4;       // BFS region sites per thread
-constexpr int REGMAX = SPT * BLOCK;   // BFS region sites per tile (tile + halo)
+constexpr int SPT1 = 4;      // BFS region sites per thread at one word per site
+constexpr int REGMAX = SPT1 * BLOCK;   // BFS region words per tile (tile + halo, x words per site)
 constexpr size_t SMEM_BYTES = (size_t)(2 + 13) * REGMAX * sizeof(uint32_t);   // frontier x2 + arc masks
+// region sites per tile for NW words per site
+__host__ __device__ constexpr int region_sites(int nw) { return REGMAX / nw; }
 
 struct Geo {
     int TY, TX, ny, nx, ntiles, H;
@@ -100,18 +104,20 @@ __device__ __forceinline__ void for_tile_groups(const Prob &p, const TileBox &tb
 
 // ---------------------------------------------------------------------------
 // one BFS round on a tile: H levels from depth d.  Returns bit0 = new interior
-// nodes, bit1 = a new interior node holds excess.  The region's 13 arc-mask
-// words per site live in shared memory (sM, REGMAX stride); they are loaded
-// when load_masks is set -- once per sweep when every CTA owns one tile.
-template <int LP, bool WIN>
+// nodes, bit1 = a new interior node holds excess.  The region's 13 x NW arc-mask
+// words per site live in shared memory; they are loaded when load_masks is set
+// -- once per sweep when every CTA owns one tile.  Word w of region site i is
+// at [w * RS + i] (RS = region_sites(NW)).
+template <int LPT, int NW, bool WIN>
 __device__ unsigned bfs_round(const Prob &p, const Arr3 &a, const Bits2 &b, const Geo &g, const TileBox &tb,
                               const uint32_t *Fin, uint32_t *Fout, const uint32_t *Vin, uint32_t *Vout, int d,
                               uint32_t *sF0, uint32_t *sF1, uint32_t *sM, bool load_masks) {
+    constexpr int RS = region_sites(NW), SPT = RS / BLOCK;
     const int P = p.P, H = g.H;
     const int ry0 = max(tb.y0 - H, 0), ry1 = min(tb.y1 + H, p.Y);
     const int rx0 = max(tb.x0 - H, 0), rx1 = min(tb.x1 + H, p.G);
     const int RW = rx1 - rx0, nreg = (ry1 - ry0) * RW;
-    uint32_t V[SPT], EX[SPT], RNG[SPT];
+    BW<NW> V[SPT], EX[SPT], RNG[SPT];
     int C[SPT];
     bool IN_[SPT];
     unsigned NB[SPT];   // neighbour-in-region bits: right, left, down, up
@@ -127,14 +133,18 @@ __device__ unsigned bfs_round(const Prob &p, const Arr3 &a, const Bits2 &b, cons
         NB[k] = (rj + 1 < RW ? 1u : 0u) | (rj > 0 ? 2u : 0u) | (i + RW < nreg ? 4u : 0u) | (ri > 0 ? 8u : 0u);
         if (load_masks && ok) {
 #pragma unroll
-            for (int q = 0; q < 13; ++q) sM[q * REGMAX + i] = b.mask[(size_t)q * P + c];
+            for (int q = 0; q < 13 * NW; ++q) sM[q * RS + i] = b.mask[(size_t)q * P + c];
         }
-        V[k] = ok ? Vin[c] : 0u;
-        EX[k] = IN_[k] ? b.EX[c] : 0u;
-        int lo = 0, hi = p.L;
-        if (WIN && ok) { lo = p.lo[c]; hi = p.hi[c]; }
-        RNG[k] = ok ? BW<1>::range(lo, hi).w[0] : 0u;
-        if (ok) sF0[i] = Fin[c];
+        V[k].zero(); EX[k].zero(); RNG[k].zero();
+        if (ok) {
+            V[k].load(Vin, P, c);
+            if (IN_[k]) EX[k].load(b.EX, P, c);
+            int lo = 0, hi = p.L;
+            if (WIN) { lo = p.lo[c]; hi = p.hi[c]; }
+            RNG[k] = BW<NW>::range(lo, hi);
+#pragma unroll
+            for (int w = 0; w < NW; ++w) sF0[w * RS + i] = Fin[(size_t)w * P + c];
+        }
     }
     __syncthreads();
     unsigned flags = 0;
@@ -144,33 +154,55 @@ __device__ unsigned bfs_round(const Prob &p, const Arr3 &a, const Bits2 &b, cons
         for (int k = 0; k < SPT; ++k) {
             const int i = threadIdx.x + k * blockDim.x;
             if (C[k] < 0) continue;
-            const uint32_t F = cur[i];
-            const uint32_t Fn0 = (NB[k] & 1u) ? cur[i + 1] : 0u;
-            const uint32_t Fn1 = (NB[k] & 2u) ? cur[i - 1] : 0u;
-            const uint32_t Fn2 = (NB[k] & 4u) ? cur[i + RW] : 0u;
-            const uint32_t Fn3 = (NB[k] & 8u) ? cur[i - RW] : 0u;
-            if ((F | Fn0 | Fn1 | Fn2 | Fn3) == 0u) {   // no frontier next to this site
-                nxt[i] = 0u;
+            BW<NW> F, Fn[4];
+            uint32_t any = 0u;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                const uint32_t *cw = cur + w * RS + i;
+                F.w[w] = cw[0];
+                Fn[0].w[w] = (NB[k] & 1u) ? cw[1] : 0u;
+                Fn[1].w[w] = (NB[k] & 2u) ? cw[-1] : 0u;
+                Fn[2].w[w] = (NB[k] & 4u) ? cw[RW] : 0u;
+                Fn[3].w[w] = (NB[k] & 8u) ? cw[-RW] : 0u;
+                any |= F.w[w] | Fn[0].w[w] | Fn[1].w[w] | Fn[2].w[w] | Fn[3].w[w];
+            }
+            if (any == 0u) {   // no frontier next to this site
+#pragma unroll
+                for (int w = 0; w < NW; ++w) nxt[w * RS + i] = 0u;
                 continue;
             }
-            const uint32_t *m = sM + i;
-            uint32_t N = (F << 1) | ((F >> 1) & m[A_UP * REGMAX]);
-            N |= (Fn0 & m[A_SR * REGMAX]) | ((Fn0 << 1) & m[A_DR * REGMAX]) | ((Fn0 >> 1) & m[A_UR * REGMAX]);
-            N |= (Fn1 & m[A_SL * REGMAX]) | ((Fn1 << 1) & m[A_DL * REGMAX]) | ((Fn1 >> 1) & m[A_UL * REGMAX]);
-            N |= (Fn2 & m[A_SD * REGMAX]) | ((Fn2 << 1) & m[A_DD * REGMAX]) | ((Fn2 >> 1) & m[A_UD * REGMAX]);
-            N |= (Fn3 & m[A_SU * REGMAX]) | ((Fn3 << 1) & m[A_DU * REGMAX]) | ((Fn3 >> 1) & m[A_UU * REGMAX]);
-            N &= RNG[k] & ~V[k];
-            V[k] |= N;
-            nxt[i] = N;
-            if (IN_[k] && N) {
+            BW<NW> M0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) M0.w[w] = sM[(A_UP * NW + w) * RS + i];
+            BW<NW> N = F.shl1() | (F.shr1() & M0);
+#pragma unroll
+            for (int dir = 0; dir < 4; ++dir) {
+                if (!Fn[dir].any()) continue;
+                BW<NW> ms, md, mu;
+#pragma unroll
+                for (int w = 0; w < NW; ++w) {
+                    ms.w[w] = sM[((A_SR + dir) * NW + w) * RS + i];
+                    md.w[w] = sM[((A_DR + dir) * NW + w) * RS + i];
+                    mu.w[w] = sM[((A_UR + dir) * NW + w) * RS + i];
+                }
+                N = N | (Fn[dir] & ms) | (Fn[dir].shl1() & md) | (Fn[dir].shr1() & mu);
+            }
+            N = gz2::andnot(N & RNG[k], V[k]);
+            V[k] = V[k] | N;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) nxt[w * RS + i] = N.w[w];
+            if (IN_[k] && N.any()) {
                 flags |= 1u;
-                if (N & EX[k]) flags |= 2u;
-                uint32_t x = N;
-                const int base = C[k] * LP;
-                while (x) {
-                    const int bb = __ffs(x) - 1;
-                    x &= x - 1;
-                    a.h[base + bb] = d + lev + 1;
+                if ((N & EX[k]).any()) flags |= 2u;
+                const int base = C[k] * LPT;
+#pragma unroll
+                for (int w = 0; w < NW; ++w) {
+                    uint32_t x = N.w[w];
+                    while (x) {
+                        const int bb = __ffs(x) - 1;
+                        x &= x - 1;
+                        a.h[base + 32 * w + bb] = d + lev + 1;
+                    }
                 }
             }
         }
@@ -181,22 +213,27 @@ __device__ unsigned bfs_round(const Prob &p, const Arr3 &a, const Bits2 &b, cons
     for (int k = 0; k < SPT; ++k) {
         if (!IN_[k]) continue;
         const int i = threadIdx.x + k * blockDim.x;
-        Fout[C[k]] = cur[i];
-        Vout[C[k]] = V[k];
+#pragma unroll
+        for (int w = 0; w < NW; ++w) Fout[(size_t)w * P + C[k]] = cur[w * RS + i];
+        V[k].store(Vout, P, C[k]);
     }
     __syncthreads();   // shared buffers are reused by the next tile
     return flags;
 }
 
 // ---------------------------------------------------------------------------
-template <int LP, bool WIN>
+// The solver.  LP = 16: two sites per warp group (m <= 16); LP = 32: one
+// (segment, site) per warp group, R segments per chain (m <= 32 R).
+template <int LP, int R, bool WIN>
 __global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b, Arr3 a, Geo g, unsigned long long *bar) {
+    constexpr int NW = R, LPT = LP * R;
     __shared__ unsigned s_f3[3], s_r3[3];
     extern __shared__ uint32_t s_dyn[];
     if (threadIdx.x < 3) { s_f3[threadIdx.x] = 0u; s_r3[threadIdx.x] = 0u; }
     __syncthreads();
     int phase = 0;
-    uint32_t *sF0 = s_dyn, *sF1 = s_dyn + REGMAX, *sM = s_dyn + 2 * REGMAX;
+    constexpr int RS = region_sites(NW);
+    uint32_t *sF0 = s_dyn, *sF1 = s_dyn + NW * RS, *sM = s_dyn + 2 * NW * RS;
     const bool resident = g.ntiles <= (int)gridDim.x;   // one tile per CTA: masks stay in smem for the sweep
     const Team tm{bar, (int)gridDim.x, (int)blockIdx.x};
 #define TEAM_SYNC() (void)tm.sync_or(0u, phase, s_f3, s_r3)
@@ -211,17 +248,42 @@ __global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b,
     volatile unsigned long long *vctr = p.ctr;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     constexpr int CPW = 32 / LP;
-    const int ngroups = (p.P + CPW - 1) / CPW;
+    const int nwords = NW * p.P;   // one bit word per (segment, site)
+    // warp groups: LP = 16 -> pairs of sites; LP = 32 -> (segment, site) words
+    const int ngroups = LP == 16 ? (p.P + 1) / 2 : nwords;
     const int gnw = tm.nb * nwarps, gwid = tm.rank * nwarps + warp;
     const int giter = (ngroups + gnw - 1) / gnw;
     const int ttid = tm.rank * blockDim.x + threadIdx.x, tstride = tm.nb * blockDim.x;
-    long long updates = 0;   // groups processed by pulses (x CPW x L = node updates)
+    long long updates = 0;   // groups processed by pulses (x CPW x LP nodes)
+
+    // Scan this warp's interleaved groups (group it0+lane), 32 per step, and run
+    // `fn(c_base, seg)` on those whose word(s) in `w1 | w2` are nonzero.
+#define FOR_ACTIVE_GROUPS(W1, W2, CNT, FN)                                                         \
+    for (int it0 = 0; it0 < giter; it0 += 32) {                                                  \
+        const int it_ = it0 + lane;                                                              \
+        const int grp_ = gwid + it_ * gnw;                                                       \
+        uint32_t wk_ = 0u;                                                                       \
+        if (it_ < giter && grp_ < ngroups) {                                                     \
+            const int w0_ = LP == 16 ? 2 * grp_ : grp_;                                          \
+            wk_ = (W1)[w0_] | (W2)[w0_];                                                         \
+            if (LP == 16 && w0_ + 1 < p.P) wk_ |= (W1)[w0_ + 1] | (W2)[w0_ + 1];                 \
+        }                                                                                        \
+        uint32_t msk_ = __ballot_sync(FULL, wk_ != 0u);                                          \
+        CNT += __popc(msk_);                                                                     \
+        while (msk_) {                                                                           \
+            const int k_ = __ffs(msk_) - 1;                                                      \
+            msk_ &= msk_ - 1;                                                                    \
+            const int gg_ = gwid + (it0 + k_) * gnw;                                             \
+            const int cb_ = LP == 16 ? 2 * gg_ : gg_ % p.P, sg_ = LP == 16 ? 0 : gg_ / p.P;      \
+            FN(cb_, sg_);                                                                        \
+        }                                                                                        \
+    }
 
     FOR_TILES {
         const TileBox tb(p, g, tile);
-        for_tile_groups<LP>(p, tb, [&](int cb, int ns) { gz3::w_init<LP, WIN>(p, a, b, cb, ns, flow, offset, presat); });
+        for_tile_groups<LP>(p, tb, [&](int cb, int ns) { gz3::w_init<LP, R, WIN>(p, a, cb, ns, flow, offset, presat); });
     }
-    for (int c = ttid; c < p.P; c += tstride) b.IN[c] = 1u;   // every site starts dirty
+    for (int w = ttid; w < nwords; w += tstride) b.IN[w] = 1u;   // every site starts dirty
     TEAM_SYNC();
     TICK(0);
     int sweeps = 0, levels_total = 0, pulses = 0, parity = 0;
@@ -230,34 +292,26 @@ __global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b,
     const int bfs_min = p.bfs_cap > 0 ? p.bfs_cap : (1 << 30);
     for (;;) {
         // ---- sweep set-up: bulk coalesced resets, then arc masks of dirty sites only ----
-        for (int c = ttid; c < p.P; c += tstride) {
+        for (int w = ttid; w < nwords; w += tstride) {
+            const int c = w % p.P, s = w / p.P;
             const int hi = WIN ? p.hi[c] : p.L;
-            b.F0[c] = BW<1>::range(hi, p.M).w[0];
-            b.V[c] = 0u;
+            b.F0[w] = BW<NW>::range(hi, p.M).w[s];
+            b.V[w] = 0u;
         }
         {
             const int4 hinf4 = make_int4(HINF, HINF, HINF, HINF);
             int4 *h4 = reinterpret_cast<int4 *>(a.h);
-            const int n4 = p.P * (LP / 4);
+            const int n4 = p.P * (LPT / 4);
             for (int q = ttid; q < n4; q += tstride) h4[q] = hinf4;
         }
-        for (int it0 = 0; it0 < giter; it0 += 32) {
-            const int it = it0 + lane;
-            const int grp = gwid + it * gnw;
-            uint32_t wk = 0u;
-            if (it < giter && grp < ngroups) {
-                const int c0 = grp * CPW;
-                wk = b.IN[c0];
-                if (CPW == 2 && c0 + 1 < p.P) wk |= b.IN[c0 + 1];
-            }
-            uint32_t msk = __ballot_sync(FULL, wk != 0u);
-            while (msk) {
-                const int k = __ffs(msk) - 1;
-                msk &= msk - 1;
-                const int c0 = (gwid + (it0 + k) * gnw) * CPW;
-                gz3::w_build<LP, WIN, false>(p, a, b, c0, CPW);
-                if (lane < CPW && c0 + lane < p.P) b.IN[c0 + lane] = 0u;
-            }
+        {
+            long long dummy = 0;
+            auto build = [&](int cb, int sg) {
+                gz3::w_build<LP, R, WIN>(p, a, b, cb, CPW, sg);
+                const int w0 = sg * p.P + cb;
+                if (lane < CPW && cb + lane < p.P) b.IN[w0 + lane] = 0u;
+            };
+            FOR_ACTIVE_GROUPS(b.IN, b.IN, dummy, build)
         }
         TEAM_SYNC();
         TICK(1);
@@ -269,7 +323,8 @@ __global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b,
             unsigned flags = 0;
             FOR_TILES {
                 const TileBox tb(p, g, tile);
-                flags |= bfs_round<LP, WIN>(p, a, b, g, tb, Fin, Fout, Vin, Vout, d, sF0, sF1, sM, d == 0 || !resident);
+                flags |= bfs_round<LPT, NW, WIN>(p, a, b, g, tb, Fin, Fout, Vin, Vout, d, sF0, sF1, sM,
+                                                 d == 0 || !resident);
             }
             const unsigned gf = TEAM_OR(flags);
             found |= (gf & 2u) != 0;
@@ -285,16 +340,7 @@ __global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b,
         if (err) break;
         if (!found && exhausted) break;
         if (p.capped && sweeps >= p.max_sweeps) { converged = 0; break; }
-        FOR_TILES {
-            const TileBox tb(p, g, tile);
-            for (int r = tb.y0 + warp; r < tb.y1; r += nwarps) {
-                const int x = tb.x0 + lane;
-                if (x < tb.x1) {
-                    const int c = r * p.G + x;
-                    b.A[c] = Vin[c] & b.EX[c];
-                }
-            }
-        }
+        for (int w = ttid; w < nwords; w += tstride) b.A[w] = Vin[w] & b.EX[w];
         TEAM_SYNC();
         for (int pulse = 0; pulse < p.K; ++pulse) {
             // Pulses are NOT tile-owned: active chains cluster spatially, so groups are
@@ -302,30 +348,19 @@ __global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b,
             // a warp checks the i-th of the warp's groups in one load; only groups with
             // active or inbox bits run a pulse.
             const uint32_t *IN_prev = parity ? a.IN0 : a.IN1;
-            for (int it0 = 0; it0 < giter; it0 += 32) {
-                const int it = it0 + lane;
-                const int grp = gwid + it * gnw;
-                uint32_t wk = 0u;
-                if (it < giter && grp < ngroups) {
-                    const int c0 = grp * CPW;
-                    wk = b.A[c0] | IN_prev[c0];
-                    if (CPW == 2 && c0 + 1 < p.P) wk |= b.A[c0 + 1] | IN_prev[c0 + 1];
-                }
-                uint32_t msk = __ballot_sync(FULL, wk != 0u);
-                updates += __popc(msk);
-                while (msk) {
-                    const int k = __ffs(msk) - 1;
-                    msk &= msk - 1;
-                    const int g2 = gwid + (it0 + k) * gnw;
-                    gz3::w_pulse<LP, WIN, false>(p, a, b, g2 * CPW, CPW, parity, flow, pushes, relabels, b.IN);
-                }
-            }
+            auto pulse_fn = [&](int cb, int sg) {
+                gz3::w_pulse<LP, R, WIN>(p, a, b, cb, CPW, sg, parity, flow, pushes, relabels, b.IN);
+            };
+            FOR_ACTIVE_GROUPS(b.A, IN_prev, updates, pulse_fn)
             TEAM_SYNC();
             parity ^= 1;
             ++pulses;
         }
         TICK(3);
         ++sweeps;
+        if (p.trace && threadIdx.x == 0 && tm.rank == 0)
+            printf("gz_trace sweep %d levels %d pulses %d t %.3f ms bfs %.3f pulses %.3f\n", sweeps, d, pulses,
+                   (gz2::gtimer() - p.t_start_ns) * 1e-6, t_acc[2] * 1e-6, t_acc[3] * 1e-6);
         {
             unsigned stop = 0;
             if (threadIdx.x == 0 && tm.rank == 0 && gz2_watchdog_expired(p)) stop = 1;
@@ -336,18 +371,19 @@ __global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b,
         }
         if (sweeps > 1000000) { if (threadIdx.x == 0 && tm.rank == 0) vctr[CTR_STATUS] = (unsigned long long)(-GZ_ERR_NOCONVERGE); break; }
     }
+#undef FOR_ACTIVE_GROUPS
     // ---- extraction: prefix closure from the excess nodes ----
 #define FOR_TILE_SITES                                                              \
     FOR_TILES                                                                       \
     for (int r = TileBox(p, g, tile).y0 + warp, y1_ = TileBox(p, g, tile).y1; r < y1_; r += nwarps) \
         for (int x = TileBox(p, g, tile).x0 + lane, x1_ = TileBox(p, g, tile).x1; x < x1_; x += 32)
-    FOR_TILE_SITES gz3::w_reach_init<WIN>(p, b, r * p.G + x);
+    FOR_TILE_SITES gz3::w_reach_init<R, WIN>(p, b, r * p.G + x);
     TEAM_SYNC();
     int reach_passes = 0;
     int32_t *Rin = b.R0, *Rout = b.R1;
     for (;;) {
         unsigned ch = 0;
-        FOR_TILE_SITES ch |= gz2::bit_reach_iter<WIN, 1>(p, b, r * p.G + x, Rin, Rout) ? 1u : 0u;
+        FOR_TILE_SITES ch |= gz2::bit_reach_iter<WIN, NW>(p, b, r * p.G + x, Rin, Rout) ? 1u : 0u;
         const bool any = TEAM_OR(ch) != 0;
         int32_t *t = Rin; Rin = Rout; Rout = t;
         ++reach_passes;
@@ -360,12 +396,12 @@ __global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b,
         const int c = r * p.G + x;
         const int lo = WIN ? p.lo[c] : 0;
         p.labels[c] = lo + Rin[c];
-        stranded += __popc(b.EX[c]);
+        for (int w = 0; w < NW; ++w) stranded += __popc(b.EX[(size_t)w * p.P + c]);
     }
     TEAM_SYNC();
     long long energy = 0;
     int viol = 0;
-    FOR_TILE_SITES gz3::w_energy<LP>(p, a, r * p.G + x, energy, viol);
+    FOR_TILE_SITES gz3::w_energy<LPT>(p, a, r * p.G + x, energy, viol);
 #undef FOR_TILE_SITES
 #undef FOR_TILES
 #undef TEAM_SYNC
@@ -381,7 +417,7 @@ __global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b,
     warp_add_u64(&p.ctr[CTR_RELABELS], relabels);
     warp_add_u64(&p.ctr[CTR_ENERGY], energy);
     warp_add_u64(&p.ctr[CTR_STRANDED], stranded);
-    if (lane == 0 && updates) atomicAdd(&p.ctr[CTR_UPDATES], (unsigned long long)updates * CPW * p.L);
+    if (lane == 0 && updates) atomicAdd(&p.ctr[CTR_UPDATES], (unsigned long long)updates * CPW * (LP < p.L ? LP : p.L));
     if (viol) p.ctr[CTR_HARDVIOL] = 1;
     if (threadIdx.x == 0 && tm.rank == 0) {
         p.ctr[CTR_SWEEPS] = sweeps;

@@ -6,19 +6,7 @@ import numpy as np, torch
 import paper_1803_01516_b200 as gz
 from paper_1803_01516_b200 import _lib, _dev
 
-def run(net, K, cap, flags=0):
-    rows, cols = net.site_shape
-    L = _lib.lib()
-    nb = L.gz_workspace_bytes(rows, cols, net.num_labels)
-    ws = _dev.workspace(nb)
-    lab = torch.empty(rows * cols, dtype=torch.int32, device="cuda")
-    st = _lib.Stats()
-    en = net.params._c()
-    sc = _lib.Sched(K, 0, cap, flags)
-    rc = L.gz_solve_volume(_dev.ptr(net.volume), rows, cols, net.num_labels, C.byref(en), C.byref(sc), None, None,
-                           _dev.ptr(lab), C.byref(st), _dev.ptr(ws), nb, _dev.stream_ptr())
-    _lib.check(rc, "solve")
-    return lab.cpu().numpy(), st
+from _solve import run
 
 seeds = [int(s) for s in sys.argv[1].split(",")]
 Hs = [int(x) for x in sys.argv[2].split(",")]
@@ -30,8 +18,8 @@ for seed in seeds:
     cub = gz.cuboid_from_disparity_range(384, 288, 10, 28, num_labels=m)
     vol = gz.sad_volume(sc.left, sc.right, cub)
     net = gz.build_network(vol, gz.EnergyParams(14, 1023))
-    ref_lab, ref = run(net, 12, 64, _lib.GZ_SCHED_V3)
-    print(f"seed {seed} v3 ref: {ref.ms_total:.2f} ms flow {ref.flow}", flush=True)
+    ref_lab, ref = run(net, 12, 0, _lib.GZ_SCHED_V2)
+    print(f"seed {seed} v2 ref: {ref.ms_total:.2f} ms flow {ref.flow}", flush=True)
     for H, cap, K in itertools.product(Hs, caps, Ks):
         os.environ["GZ_BFS_H"] = str(H)
         best = None
