@@ -857,9 +857,21 @@ gz4::Geo tile_geo(int rows, int cols, int nb, int nw) {
 }
 
 // Solve one problem whose volume is already in w.vol (layout of the chosen solver).
-int solve_planar(const Workspace &w, int rows, int cols, int m, const gz_energy *en, const gz_sched *sc,
-                 const int32_t *lo, const int32_t *hi, int32_t *labels_out, gz_stats *st, cudaStream_t s,
-                 int hcap = HARD_CAP_DEFAULT) {
+// A launched, not yet collected solve.
+struct Pending {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    unsigned long long *h_ctr = nullptr;   // counters copied back (pinned for asynchronous use)
+    int hard = 0, hcap = 0;
+    volatile unsigned *progress = nullptr;
+    int grid = 0;
+};
+
+// Enqueue one solve of the problem whose volume is already in w.vol (layout of
+// the chosen solver) on stream s, using 1/conc of the SMs.  Counters go to
+// h_ctr, labels to labels_out; collect with solve_finish after the stream.
+int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy *en, const gz_sched *sc,
+                 const int32_t *lo, const int32_t *hi, int32_t *labels_out, cudaStream_t s, int hcap, int conc,
+                 unsigned long long *h_ctr, Pending *pd) {
     Prob p;
     memset(&p, 0, sizeof(p));
     p.Y = rows; p.G = cols; p.M = m; p.L = m - 1; p.P = rows * cols;
@@ -880,10 +892,12 @@ int solve_planar(const Workspace &w, int rows, int cols, int m, const gz_energy 
     p.e = w.e; p.ein = w.ein; p.h = w.h; p.h2 = w.h2; p.reach = w.reach; p.reach2 = w.reach2; p.labels = w.labels;
     p.ctr = w.ctr;
     CK(cudaMemsetAsync(w.ctr, 0, gz::CTR_COUNT * 8, s));
-    cudaEvent_t e0, e1;
-    CK(cudaEventCreate(&e0));
-    CK(cudaEventCreate(&e1));
-    CK(cudaEventRecord(e0, s));
+    CK(cudaEventCreate(&pd->e0));
+    CK(cudaEventCreate(&pd->e1));
+    pd->h_ctr = h_ctr;
+    pd->hard = p.hard;
+    pd->hcap = p.hcap;
+    CK(cudaEventRecord(pd->e0, s));
     const bool win = lo != nullptr;
     const int NW = words_for(m);
     const bool det = p.capped != 0;
@@ -917,6 +931,7 @@ int solve_planar(const Workspace &w, int rows, int cols, int m, const gz_energy 
     int grid = 0;
     int rc = coop_grid(kern, threads, &grid, dyn_smem);
     if (rc) return rc;
+    if (conc > 1) grid = grid / conc > 0 ? grid / conc : 1;
     const int need = (p.P + 255) / 256;
     if (grid > need) grid = need < 1 ? 1 : need;
     gz4::Geo geo{};
@@ -942,35 +957,28 @@ int solve_planar(const Workspace &w, int rows, int cols, int m, const gz_energy 
     } else {
         CK(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(256), which == 1 ? args1 : args2, 0, s));
     }
-    CK(cudaEventRecord(e1, s));
-    if (p.progress) {   // debug: poll instead of blocking, report where blocks stall
-        const double limit = atof(getenv("GZ_DEBUG_PROGRESS"));
-        const double t0 = (double)clock() / CLOCKS_PER_SEC;
-        while (cudaEventQuery(e1) == cudaErrorNotReady) {
-            if ((double)clock() / CLOCKS_PER_SEC - t0 > limit) {
-                fprintf(stderr, "gazecut_b200: solve still running after %.1fs; per-block phase counters:\n", limit);
-                for (int i = 0; i < grid; ++i) fprintf(stderr, "%u%c", p.progress[i], (i % 32 == 31) ? '\n' : ' ');
-                fprintf(stderr, "\n");
-                fflush(stderr);
-                _exit(3);
-            }
-        }
-    }
-    unsigned long long h_ctr[gz::CTR_COUNT];
-    CK(cudaMemcpyAsync(h_ctr, w.ctr, sizeof(h_ctr), cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(pd->e1, s));
+    pd->progress = p.progress;
+    pd->grid = grid;
+    CK(cudaMemcpyAsync(h_ctr, w.ctr, gz::CTR_COUNT * 8, cudaMemcpyDeviceToHost, s));
     if (labels_out && labels_out != w.labels)
         CK(cudaMemcpyAsync(labels_out, w.labels, (size_t)p.P * 4, cudaMemcpyDeviceToDevice, s));
-    CK(cudaStreamSynchronize(s));
+    return GZ_OK;
+}
+
+// Collect a solve once its stream has completed.
+int solve_finish(Pending &pd, gz_stats *st) {
     float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, e0, e1));
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+    CK(cudaEventElapsedTime(&ms, pd.e0, pd.e1));
+    cudaEventDestroy(pd.e0);
+    cudaEventDestroy(pd.e1);
+    const unsigned long long *h_ctr = pd.h_ctr;
     if (h_ctr[CTR_STATUS]) return -(int)h_ctr[CTR_STATUS];
     if (st) {
         memset(st, 0, sizeof(*st));
         st->flow = (int64_t)h_ctr[CTR_FLOW];
-        if (p.hard) {   // rescale uncuttable multiples to the reference's 2^56 (see gz_graph.cuh)
-            const int64_t k = st->flow / p.hcap, f = st->flow % p.hcap;
+        if (pd.hard) {   // rescale uncuttable multiples to the reference's 2^56 (see gz_graph.cuh)
+            const int64_t k = st->flow / pd.hcap, f = st->flow % pd.hcap;
             st->flow = k * (int64_t)gz::UNCUTTABLE + f;
         }
         st->const_offset = (int64_t)h_ctr[CTR_OFFSET];
@@ -990,6 +998,31 @@ int solve_planar(const Workspace &w, int rows, int cols, int m, const gz_energy 
         for (int q = 0; q < 6; ++q) st->ms_phase[q] = (float)(h_ctr[CTR_T0 + q] * 1e-6);
     }
     return GZ_OK;
+}
+
+// Synchronous solve (one problem, all SMs).
+int solve_planar(const Workspace &w, int rows, int cols, int m, const gz_energy *en, const gz_sched *sc,
+                 const int32_t *lo, const int32_t *hi, int32_t *labels_out, gz_stats *st, cudaStream_t s,
+                 int hcap = HARD_CAP_DEFAULT) {
+    unsigned long long h_ctr[gz::CTR_COUNT];
+    Pending pd;
+    int rc = solve_launch(w, rows, cols, m, en, sc, lo, hi, labels_out, s, hcap, 1, h_ctr, &pd);
+    if (rc) return rc;
+    if (pd.progress) {   // debug: poll instead of blocking, report where blocks stall
+        const double limit = atof(getenv("GZ_DEBUG_PROGRESS"));
+        const double t0 = (double)clock() / CLOCKS_PER_SEC;
+        while (cudaEventQuery(pd.e1) == cudaErrorNotReady) {
+            if ((double)clock() / CLOCKS_PER_SEC - t0 > limit) {
+                fprintf(stderr, "gazecut_b200: solve still running after %.1fs; per-block phase counters:\n", limit);
+                for (int i = 0; i < pd.grid; ++i) fprintf(stderr, "%u%c", pd.progress[i], (i % 32 == 31) ? '\n' : ' ');
+                fprintf(stderr, "\n");
+                fflush(stderr);
+                _exit(3);
+            }
+        }
+    }
+    CK(cudaStreamSynchronize(s));
+    return solve_finish(pd, st);
 }
 
 int check_sm100() {
@@ -1089,25 +1122,80 @@ int gz_solve_pairs(const uint8_t *left, const uint8_t *right, int32_t batch, int
     if (workspace_bytes < one) return GZ_ERR_WORKSPACE;
     int rc = check_sm100();
     if (rc) return rc;
+    // SAD costs are <= 255*channels, which bounds the total source capacity
+    const unsigned long long fin = (unsigned long long)P * 255ull * (unsigned long long)channels;
+    if (fin >= (energy->hard_inhibit ? (1ull << 29) : 0x7fffffffull)) return GZ_ERR_OVERFLOW;
     cudaStream_t s = (cudaStream_t)stream;
-    Workspace w = carve(workspace, rows, cols, m);
     const size_t img = (size_t)img_h * img_w * channels;
-    for (int b = 0; b < batch; ++b) {
-        const int which = choose_solver(m, sched);
-        if (which == 4)
-            k_sad<2><<<(P + 127) / 128, 128, 0, s>>>(left + b * img, right + b * img, img_w, channels, *cb, w.vol,
-                                                     lanes_for(m));
-        else
-            k_sad<1><<<(P + 127) / 128, 128, 0, s>>>(left + b * img, right + b * img, img_w, channels, *cb, w.vol);
-        CK(cudaGetLastError());
-        // SAD costs are <= 255*channels, which bounds the total source capacity
-        const unsigned long long fin = (unsigned long long)P * 255ull * (unsigned long long)channels;
-        if (fin >= (energy->hard_inhibit ? (1ull << 29) : 0x7fffffffull)) return GZ_ERR_OVERFLOW;
-        rc = solve_planar(w, rows, cols, m, energy, sched, nullptr, nullptr, labels_out + (size_t)b * P,
-                          stats_out ? stats_out + b : nullptr, s, 1 << 30);
-        if (rc) return rc;
-        if (stats_out && stats_out[b].energy != stats_out[b].labeling_energy) return GZ_ERR_CONSISTENCY;
+    const int which = choose_solver(m, sched);
+    // Concurrent solves: up to `conc` pairs run at once, each a cooperative launch
+    // over 1/conc of the SMs on its own stream with its own workspace slice.
+    int conc = 2;
+    if (const char *cs = getenv("GZ_PAIR_CONC")) conc = atoi(cs);
+    if (conc > 8) conc = 8;
+    if ((size_t)conc * one > workspace_bytes) conc = (int)(workspace_bytes / one);
+    if (conc > batch) conc = batch;
+    if (which != 4 || conc < 1) conc = 1;
+    static cudaStream_t streams[8];
+    static bool have_streams = false;
+    static unsigned long long *pinned = nullptr;
+    static size_t pinned_n = 0;
+    if (conc > 1 && !have_streams) {
+        for (int k = 0; k < 8; ++k) CK(cudaStreamCreateWithFlags(&streams[k], cudaStreamNonBlocking));
+        have_streams = true;
     }
+    if (pinned_n < (size_t)batch * gz::CTR_COUNT) {
+        if (pinned) cudaFreeHost(pinned);
+        pinned_n = (size_t)batch * gz::CTR_COUNT;
+        CK(cudaHostAlloc((void **)&pinned, pinned_n * 8, cudaHostAllocDefault));
+    }
+    cudaEvent_t fork = nullptr;
+    if (conc > 1) {
+        CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+        CK(cudaEventRecord(fork, s));
+        for (int k = 0; k < conc; ++k) CK(cudaStreamWaitEvent(streams[k], fork, 0));
+    }
+    Pending *pend = new Pending[batch];
+    for (int b = 0; b < batch && rc == GZ_OK; ++b) {
+        const int k = b % conc;
+        cudaStream_t sk = conc > 1 ? streams[k] : s;
+        Workspace w = carve((uint8_t *)workspace + (size_t)k * one, rows, cols, m);
+        if (which == 4)
+            k_sad<2><<<(P + 127) / 128, 128, 0, sk>>>(left + b * img, right + b * img, img_w, channels, *cb, w.vol,
+                                                      lanes_for(m));
+        else
+            k_sad<1><<<(P + 127) / 128, 128, 0, sk>>>(left + b * img, right + b * img, img_w, channels, *cb, w.vol);
+        if (cudaGetLastError() != cudaSuccess) { rc = GZ_ERR_CUDA; break; }
+        rc = solve_launch(w, rows, cols, m, energy, sched, nullptr, nullptr, labels_out + (size_t)b * P, sk, 1 << 30,
+                          conc, pinned + (size_t)b * gz::CTR_COUNT, &pend[b]);
+        if (rc) break;
+        if (conc == 1) {   // one at a time: collect now (keeps the pinned slot reuse trivial)
+            if (cudaStreamSynchronize(s) != cudaSuccess) { rc = GZ_ERR_CUDA; break; }
+            rc = solve_finish(pend[b], stats_out ? stats_out + b : nullptr);
+            pend[b].e0 = nullptr;
+        }
+    }
+    if (conc > 1) {
+        for (int k = 0; k < conc; ++k) {
+            cudaEvent_t join;
+            cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
+            cudaEventRecord(join, streams[k]);
+            cudaStreamWaitEvent(s, join, 0);
+            cudaEventDestroy(join);
+        }
+        cudaEventDestroy(fork);
+        if (cudaStreamSynchronize(s) != cudaSuccess && rc == GZ_OK) rc = GZ_ERR_CUDA;
+        for (int b = 0; b < batch; ++b) {
+            if (!pend[b].e0) continue;
+            const int r = solve_finish(pend[b], stats_out ? stats_out + b : nullptr);
+            if (rc == GZ_OK) rc = r;
+        }
+    }
+    delete[] pend;
+    if (rc) return rc;
+    if (stats_out)
+        for (int b = 0; b < batch; ++b)
+            if (stats_out[b].energy != stats_out[b].labeling_energy) return GZ_ERR_CONSISTENCY;
     return GZ_OK;
 }
 
@@ -1119,15 +1207,18 @@ int gz_solve_pairs_host(const uint8_t *left_host, const uint8_t *right_host, int
     const int P = cb->y_extent * cb->g_extent;
     const size_t img = (size_t)img_h * img_w * channels * batch;
     const size_t one = ws_bytes(cb->y_extent, cb->g_extent, cb->m);
-    const size_t need = one + 2 * align_up(img) + align_up((size_t)batch * P * 4);
-    if (workspace_bytes < need) return GZ_ERR_WORKSPACE;
+    const size_t io = 2 * align_up(img) + align_up((size_t)batch * P * 4) + 256;
+    if (workspace_bytes < one + io) return GZ_ERR_WORKSPACE;
     cudaStream_t s = (cudaStream_t)stream;
+    // device copies of the inputs / labels at the start, solver workspace after
     uint8_t *base = (uint8_t *)(((uintptr_t)workspace + 255) & ~(uintptr_t)255);
-    uint8_t *dl = base + one, *dr = dl + align_up(img);
+    uint8_t *dl = base, *dr = dl + align_up(img);
     int32_t *dlab = (int32_t *)(dr + align_up(img));
+    uint8_t *wsp = (uint8_t *)dlab + align_up((size_t)batch * P * 4);
+    const size_t ws_left = workspace_bytes - (size_t)(wsp - (uint8_t *)workspace);
     CK(cudaMemcpyAsync(dl, left_host, img, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(dr, right_host, img, cudaMemcpyHostToDevice, s));
-    int rc = gz_solve_pairs(dl, dr, batch, img_h, img_w, channels, cb, energy, sched, dlab, stats_host, base, one, s);
+    int rc = gz_solve_pairs(dl, dr, batch, img_h, img_w, channels, cb, energy, sched, dlab, stats_host, wsp, ws_left, s);
     if (rc) return rc;
     CK(cudaMemcpyAsync(labels_host, dlab, (size_t)batch * P * 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));

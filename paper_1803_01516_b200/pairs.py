@@ -52,9 +52,12 @@ class PairSolver:
         self.sites = cuboid.y_extent * cuboid.g_extent
         self.ws_one = _lib.lib().gz_workspace_bytes(cuboid.y_extent, cuboid.g_extent, cuboid.num_labels)
         self._ws: Optional[torch.Tensor] = None
+        self.concurrency = 8
 
-    def _workspace(self, extra: int = 0) -> torch.Tensor:
-        need = self.ws_one + extra + 4096
+    def _workspace(self, extra: int = 0, batch: int = 1) -> torch.Tensor:
+        # room for up to `concurrency` pair solves in flight (gz_solve_pairs runs
+        # that many cooperative launches side by side, each on 1/k of the SMs)
+        need = self.ws_one * max(1, min(batch, self.concurrency)) + extra + 4096
         if self._ws is None or self._ws.numel() < need:
             self._ws = torch.empty(need, dtype=torch.uint8, device=self.dev)
         return self._ws
@@ -73,7 +76,7 @@ class PairSolver:
         if labels is None:
             labels = torch.empty((b, self.cuboid.y_extent, self.cuboid.g_extent), dtype=torch.int32, device=self.dev)
         stats = (_lib.Stats * b)()
-        ws = self._workspace()
+        ws = self._workspace(0, b)
         rc = _lib.lib().gz_solve_pairs(_dev.ptr(left), _dev.ptr(right), b, self.h, self.w, self.ch,
                                        C.byref(self.cs), C.byref(self.en), C.byref(self.sc), _dev.ptr(labels),
                                        stats, _dev.ptr(ws), ws.numel(), _dev.stream_ptr())
@@ -93,7 +96,7 @@ class PairSolver:
             labels = np.empty((b, self.cuboid.y_extent, self.cuboid.g_extent), np.int32)
         img = left[0].nbytes
         extra = 2 * (b * img + 256) + b * self.sites * 4 + 256
-        ws = self._workspace(extra)
+        ws = self._workspace(extra, b)
         stats = (_lib.Stats * b)()
         rc = _lib.lib().gz_solve_pairs_host(
             left.ctypes.data_as(C.c_void_p), right.ctypes.data_as(C.c_void_p), b, self.h, self.w, self.ch,
