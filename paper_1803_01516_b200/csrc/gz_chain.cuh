@@ -351,41 +351,37 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
             }
         }
     }
-    // lateral and downward pushes of the remaining excess
-    int dn = 0;
-    int ph_d = 0, pv_d = 0, dar_d = 0, dad_d = 0;
-    int phL_d = 0, pvU_d = 0, dbrL_d = 0, dbdU_d = 0, dbr_up_d = 0, darL_up_d = 0, dbd_up_d = 0, dadU_up_d = 0;
-    if (live && e > 0) {
+    // lateral and downward pushes of the remaining excess: admissible residuals
+    // in push order, then a short min/subtract allocation (independent of the
+    // arc bookkeeping, which follows as predicated selects)
+    int dd[A_COUNT];
+    {
+        int rem = (live && e > 0) ? e : 0;
 #pragma unroll
         for (int jj = A_SR; jj <= A_DN; ++jj) {
-            if (e <= 0) break;
-            if (A.kd[jj] == K_SRC || A.r[jj] <= 0 || hu != A.hv[jj] + 1) continue;
-            const int d = min(e, A.r[jj]);
-            e -= d;
-            pushed = true;
-            ++pushes;
-            switch (jj) {
-            case A_SR: ph_d -= d; break;
-            case A_SL: phL_d += d; break;
-            case A_SD: pv_d -= d; break;
-            case A_SU: pvU_d += d; break;
-            case A_UR: dbr_up_d -= d; break;
-            case A_UL: darL_up_d -= d; break;
-            case A_UD: dbd_up_d -= d; break;
-            case A_UU: dadU_up_d -= d; break;
-            case A_DR: dar_d += d; break;
-            case A_DL: dbrL_d += d; break;
-            case A_DD: dad_d += d; break;
-            case A_DU: dbdU_d += d; break;
-            case A_DN: dn += d; break;
-            }
-            if (jj == A_DN) continue;
-            if (A.kd[jj] == K_SNK) { flow += d; continue; }
-            int site, pos;
-            lateral_target<LP, R, WIN>(L, jj, site, pos);
-            atomicAdd(&ein_cur[site * LPT + pos - 1], d);
-            atomicOr(&IN_cur[((pos - 1) / LP) * P + site], 1u << ((pos - 1) % LP));
+            const bool adm = A.kd[jj] != K_SRC && A.r[jj] > 0 && hu == A.hv[jj] + 1;
+            const int d = adm ? min(rem, A.r[jj]) : 0;
+            dd[jj] = d;
+            rem -= d;
         }
+        if (live && e > 0) e = rem;
+    }
+    const int ph_d = -dd[A_SR], pv_d = -dd[A_SD], dar_d = dd[A_DR], dad_d = dd[A_DD];
+    const int phL_d = dd[A_SL], pvU_d = dd[A_SU], dbrL_d = dd[A_DL], dbdU_d = dd[A_DU];
+    const int dbr_up_d = -dd[A_UR], darL_up_d = -dd[A_UL], dbd_up_d = -dd[A_UD], dadU_up_d = -dd[A_UU];
+    const int dn = dd[A_DN];
+#pragma unroll
+    for (int jj = A_SR; jj <= A_DN; ++jj) {
+        const int d = dd[jj];
+        if (d <= 0) continue;
+        pushed = true;
+        ++pushes;
+        if (jj == A_DN) continue;
+        if (A.kd[jj] == K_SNK) { flow += d; continue; }
+        int site, pos;
+        lateral_target<LP, R, WIN>(L, jj, site, pos);
+        atomicAdd(&ein_cur[site * LPT + pos - 1], d);
+        atomicOr(&IN_cur[((pos - 1) / LP) * P + site], 1u << ((pos - 1) % LP));
     }
     // chain-down pushes arrive at lane j-1 (adds to its excess and to its chain-up
     // residual); out of a segment's first lane they cross into the segment below

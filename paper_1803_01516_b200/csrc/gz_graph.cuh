@@ -56,12 +56,14 @@ struct Prob {
     int pen, inh, hard;
     int hcap;            // stand-in capacity of uncuttable inhibit arcs (hard mode)
     int K;               // pulses per sweep
+    int k_tail, tail_after;   // v4: pulses per sweep from sweep `tail_after` on (0 = K)
     int bfs_cap;         // lateral relaxations per non-final global relabel (0 = exact)
     int max_sweeps;      // honoured when capped
     int capped;
     unsigned long long watchdog_ns, t_start_ns;   // 0 = no watchdog; start stamped on device
     volatile unsigned *progress;                  // debug: per-block phase counter (mapped host memory) or null
-    int trace;                                    // debug: per-sweep device printf (env GZ_TRACE)
+    int trace;                                    // debug: 1 per-sweep device printf, 2 per-pulse trace (env GZ_TRACE)
+    unsigned long long *tbuf;                     // debug: per-pulse (sweep|pulse|groups, ns) records
     int no_wave;         // skip the initial chain wave
     const int32_t *lo, *hi;   // windowed only
     int32_t *vol, *cu, *ph, *pv, *dar, *dbr, *dad, *dbd;
@@ -76,6 +78,7 @@ enum Ctr : int {
     CTR_FLAG0 = 16,     // 3 rotating "changed" flags
     CTR_ACT0 = 20,      // 3 rotating active counters
     CTR_T0 = 24,        // 6 phase timers (ns): init, mask build, bfs, pulses, reach, tail
+    CTR_TRACE = 35,     // debug trace accumulator (GZ_TRACE=2)
     CTR_UPDATES = 30,   // node updates performed by pulses (v4)
     CTR_BAR0 = 32,      // 3 rotating team-barrier words (v4)
     CTR_COUNT = 40

@@ -864,6 +864,7 @@ struct Pending {
     int hard = 0, hcap = 0;
     volatile unsigned *progress = nullptr;
     int grid = 0;
+    unsigned long long *tbuf = nullptr;
 };
 
 // Enqueue one solve of the problem whose volume is already in w.vol (layout of
@@ -886,7 +887,13 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
         const char *wd = getenv("GZ_WATCHDOG_MS");
         p.watchdog_ns = (unsigned long long)(wd ? atof(wd) : 20000.0) * 1000000ull;
     }
-    p.trace = getenv("GZ_TRACE") ? 1 : 0;
+    p.trace = getenv("GZ_TRACE") ? atoi(getenv("GZ_TRACE")) : 0;
+    static unsigned long long *tbuf = nullptr;
+    if (p.trace > 1) {
+        if (!tbuf) CK(cudaMalloc((void **)&tbuf, 8192 * 8));
+        CK(cudaMemsetAsync(tbuf, 0, 8192 * 8, s));
+        p.tbuf = tbuf;
+    }
     p.lo = lo; p.hi = hi;
     p.vol = w.vol; p.cu = w.cu; p.ph = w.ph; p.pv = w.pv; p.dar = w.dar; p.dbr = w.dbr; p.dad = w.dad; p.dbd = w.dbd;
     p.e = w.e; p.ein = w.ein; p.h = w.h; p.h2 = w.h2; p.reach = w.reach; p.reach2 = w.reach2; p.labels = w.labels;
@@ -908,6 +915,12 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
     // (measured: C1 m=16 best at 48 / 12, C2 m=60 at 128 / 48; tools/sweep_cfg.py)
     if (!v1 && p.bfs_cap == 0) p.bfs_cap = which == 4 ? (2 * m + 16 > 48 ? 2 * m + 16 : 48) : 64;
     if (which == 4 && !p.capped && m - 12 > p.K) p.K = m - 12;
+    if (which == 4 && !p.capped) {   // tail sweeps: few active chains, pulses are cheap next to a global relabel
+        const char *kt = getenv("GZ_KTAIL"), *ta = getenv("GZ_TAIL_AFTER");
+        // measured (tools/tail_knobs.py, C1 seeds 0-7; C2): 96 pulses from the fifth sweep on
+        p.k_tail = kt ? atoi(kt) : (p.K > 96 ? p.K : 96);
+        p.tail_after = ta ? atoi(ta) : 4;
+    }
     if (!v1 && p.bfs_cap < 0) p.bfs_cap = 0;            // exhaustive BFS every sweep
     const void *kern = nullptr;
 #define GZ_PICK(W_, NW_, D_) if (win == W_ && NW == NW_ && det == D_) kern = (const void *)gz2::gz_bitsolve_kernel<W_, NW_, D_>;
@@ -959,6 +972,7 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
     }
     CK(cudaEventRecord(pd->e1, s));
     pd->progress = p.progress;
+    pd->tbuf = p.tbuf;
     pd->grid = grid;
     CK(cudaMemcpyAsync(h_ctr, w.ctr, gz::CTR_COUNT * 8, cudaMemcpyDeviceToHost, s));
     if (labels_out && labels_out != w.labels)
@@ -968,6 +982,13 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
 
 // Collect a solve once its stream has completed.
 int solve_finish(Pending &pd, gz_stats *st) {
+    if (pd.tbuf) {   // debug: dump the per-pulse trace
+        static unsigned long long h[8192];
+        CK(cudaMemcpy(h, pd.tbuf, sizeof(h), cudaMemcpyDeviceToHost));
+        for (int i = 0; i < 4096 && h[2 * i + 1]; ++i)
+            fprintf(stderr, "gz_pulse sweep %llu pulse %llu groups %llu dt_us %.2f\n", h[2 * i] >> 48,
+                    (h[2 * i] >> 32) & 0xffff, h[2 * i] & 0xffffffffull, h[2 * i + 1] * 1e-3);
+    }
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, pd.e0, pd.e1));
     cudaEventDestroy(pd.e0);

@@ -227,9 +227,12 @@ __device__ unsigned bfs_round(const Prob &p, const Arr3 &a, const Bits2 &b, cons
 template <int LP, int R, bool WIN>
 __global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b, Arr3 a, Geo g, unsigned long long *bar) {
     constexpr int NW = R, LPT = LP * R;
-    __shared__ unsigned s_f3[3], s_r3[3];
+    __shared__ unsigned s_f3[3], s_r3[3], s_qn[2];
+    __shared__ int s_q[BLOCK];   // per-round pool of active groups (<= 32 per warp)
     extern __shared__ uint32_t s_dyn[];
     if (threadIdx.x < 3) { s_f3[threadIdx.x] = 0u; s_r3[threadIdx.x] = 0u; }
+    if (threadIdx.x < 2) s_qn[threadIdx.x] = 0u;
+    int qround = 0;
     __syncthreads();
     int phase = 0;
     constexpr int RS = region_sites(NW);
@@ -256,10 +259,13 @@ __global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b,
     const int ttid = tm.rank * blockDim.x + threadIdx.x, tstride = tm.nb * blockDim.x;
     long long updates = 0;   // groups processed by pulses (x CPW x LP nodes)
 
-    // Scan this warp's interleaved groups (group it0+lane), 32 per step, and run
-    // `fn(c_base, seg)` on those whose word(s) in `w1 | w2` are nonzero.
+    // Scan the warps' interleaved groups (group it0+lane of every warp, 32 per
+    // round), pool the ones whose word(s) in W1 | W2 are nonzero in shared memory,
+    // and deal the pool round-robin to the CTA's warps: the critical path of a
+    // phase is the busiest warp, and pooling per CTA flattens the Poisson spread
+    // of active groups across warps.  Two pool counters alternate by round.
 #define FOR_ACTIVE_GROUPS(W1, W2, CNT, FN)                                                         \
-    for (int it0 = 0; it0 < giter; it0 += 32) {                                                  \
+    for (int it0 = 0; it0 < giter; it0 += 32, ++qround) {                                        \
         const int it_ = it0 + lane;                                                              \
         const int grp_ = gwid + it_ * gnw;                                                       \
         uint32_t wk_ = 0u;                                                                       \
@@ -268,15 +274,22 @@ __global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b,
             wk_ = (W1)[w0_] | (W2)[w0_];                                                         \
             if (LP == 16 && w0_ + 1 < p.P) wk_ |= (W1)[w0_ + 1] | (W2)[w0_ + 1];                 \
         }                                                                                        \
-        uint32_t msk_ = __ballot_sync(FULL, wk_ != 0u);                                          \
+        const uint32_t msk_ = __ballot_sync(FULL, wk_ != 0u);                                    \
         CNT += __popc(msk_);                                                                     \
-        while (msk_) {                                                                           \
-            const int k_ = __ffs(msk_) - 1;                                                      \
-            msk_ &= msk_ - 1;                                                                    \
-            const int gg_ = gwid + (it0 + k_) * gnw;                                             \
+        unsigned *qn_ = s_qn + (qround & 1);                                                     \
+        int base_ = 0;                                                                           \
+        if (lane == 0 && msk_) base_ = (int)atomicAdd(qn_, (unsigned)__popc(msk_));              \
+        base_ = __shfl_sync(FULL, base_, 0);                                                     \
+        if ((msk_ >> lane) & 1u) s_q[base_ + __popc(msk_ & ((1u << lane) - 1u))] = grp_;         \
+        __syncthreads();                                                                         \
+        if (threadIdx.x == 0) s_qn[(qround + 1) & 1] = 0u;                                       \
+        const int n_ = (int)*qn_;                                                                \
+        for (int q_ = warp; q_ < n_; q_ += nwarps) {                                             \
+            const int gg_ = s_q[q_];                                                             \
             const int cb_ = LP == 16 ? 2 * gg_ : gg_ % p.P, sg_ = LP == 16 ? 0 : gg_ / p.P;      \
             FN(cb_, sg_);                                                                        \
         }                                                                                        \
+        __syncthreads();                                                                         \
     }
 
     FOR_TILES {
@@ -342,7 +355,10 @@ __global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b,
         if (p.capped && sweeps >= p.max_sweeps) { converged = 0; break; }
         for (int w = ttid; w < nwords; w += tstride) b.A[w] = Vin[w] & b.EX[w];
         TEAM_SYNC();
-        for (int pulse = 0; pulse < p.K; ++pulse) {
+        unsigned long long t_pulse = p.trace > 1 ? gz2::gtimer() : 0ull;
+        // pulses this sweep: K, or K_tail once the dense opening sweeps are over
+        const int kp = (p.k_tail > 0 && sweeps >= p.tail_after) ? p.k_tail : p.K;
+        for (int pulse = 0; pulse < kp; ++pulse) {
             // Pulses are NOT tile-owned: active chains cluster spatially, so groups are
             // interleaved over every warp of the team (group g -> warp g mod W).  Lane i of
             // a warp checks the i-th of the warp's groups in one load; only groups with
@@ -351,10 +367,22 @@ __global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b,
             auto pulse_fn = [&](int cb, int sg) {
                 gz3::w_pulse<LP, R, WIN>(p, a, b, cb, CPW, sg, parity, flow, pushes, relabels, b.IN);
             };
+            long long upd0 = updates;
             FOR_ACTIVE_GROUPS(b.A, IN_prev, updates, pulse_fn)
-            TEAM_SYNC();
+            if (p.trace > 1 && lane == 0 && updates != upd0) atomicAdd(&p.ctr[CTR_TRACE], (unsigned long long)(updates - upd0));
+            // an empty pulse (no active or inbox word anywhere) ends the sweep early
+            const bool idle = TEAM_OR(updates != upd0 ? 1u : 0u) == 0u;
+            if (p.trace > 1 && p.tbuf && threadIdx.x == 0 && tm.rank == 0 && pulses < 4096) {
+                const unsigned long long now = gz2::gtimer();
+                p.tbuf[2 * pulses] = ((unsigned long long)sweeps << 48) | ((unsigned long long)pulse << 32) |
+                                     ((volatile unsigned long long *)p.ctr)[CTR_TRACE];
+                p.tbuf[2 * pulses + 1] = now - t_pulse;
+                t_pulse = now;
+                p.ctr[CTR_TRACE] = 0ull;
+            }
             parity ^= 1;
             ++pulses;
+            if (idle) break;
         }
         TICK(3);
         ++sweeps;
