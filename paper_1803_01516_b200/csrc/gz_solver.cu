@@ -836,8 +836,8 @@ int choose_solver(int m, const gz_sched *sc) {
 }
 
 // Tile geometry of the v4 solver for a team of nb CTAs.
-gz4::Geo tile_geo(int rows, int cols, int nb, int nw) {
-    const int regmax = gz4::region_sites(nw);
+gz4::Geo tile_geo(int rows, int cols, int nb, int nw, int occ) {
+    const int regmax = gz4::region_sites(nw, occ);
     gz4::Geo g;
     const char *hs = getenv("GZ_BFS_H");
     g.H = hs ? atoi(hs) : 8;
@@ -926,9 +926,17 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
 #define GZ_PICK(W_, NW_, D_) if (win == W_ && NW == NW_ && det == D_) kern = (const void *)gz2::gz_bitsolve_kernel<W_, NW_, D_>;
 #define GZ_PICK_NW(NW_) GZ_PICK(false, NW_, false) GZ_PICK(false, NW_, true) GZ_PICK(true, NW_, false) GZ_PICK(true, NW_, true)
     const int LPn = lanes_for(m);
+    // two CTAs per SM (64 registers, smaller BFS regions) for the m <= 16 instance
+    // (spills cost ~12% on a lone solve; with concurrent pair solves the doubled
+    // warp count wins ~12%: bench A/B, round 1)
+    int occ4 = 1;
+    if (LPn == 16) {
+        const char *oc = getenv("GZ_OCC");
+        occ4 = oc ? (atoi(oc) == 2 ? 2 : 1) : (conc >= 2 ? 2 : 1);
+    }
     if (which == 4) {
-#define GZ_PICK4(LP_, R_) if (LPn == LP_ * R_) kern = win ? (const void *)gz4::gz_tilesolve_kernel<LP_, R_, true> : (const void *)gz4::gz_tilesolve_kernel<LP_, R_, false>;
-        GZ_PICK4(16, 1) GZ_PICK4(32, 1) GZ_PICK4(32, 2) GZ_PICK4(32, 4)
+#define GZ_PICK4(LP_, R_, O_) if (LPn == LP_ * R_ && occ4 == O_) kern = win ? (const void *)gz4::gz_tilesolve_kernel<LP_, R_, true, O_> : (const void *)gz4::gz_tilesolve_kernel<LP_, R_, false, O_>;
+        GZ_PICK4(16, 1, 1) GZ_PICK4(16, 1, 2) GZ_PICK4(32, 1, 1) GZ_PICK4(32, 2, 1) GZ_PICK4(32, 4, 1)
 #undef GZ_PICK4
     } else if (which == 2) {
         GZ_PICK_NW(1) GZ_PICK_NW(2) GZ_PICK_NW(4) GZ_PICK_NW(8)
@@ -939,7 +947,7 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
 #undef GZ_PICK
     if (!v1) CK(cudaMemsetAsync(w.bits_base, 0, w.bits_bytes, s));
     const int threads = which == 4 ? gz4::BLOCK : 256;
-    const size_t dyn_smem = which == 4 ? gz4::SMEM_BYTES : 0;
+    const size_t dyn_smem = which == 4 ? gz4::smem_bytes(occ4) : 0;
     if (which == 4) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem));
     int grid = 0;
     int rc = coop_grid(kern, threads, &grid, dyn_smem);
@@ -949,7 +957,7 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
     if (grid > need) grid = need < 1 ? 1 : need;
     gz4::Geo geo{};
     unsigned long long *bar = w.ctr + gz::CTR_BAR0;
-    if (which == 4) geo = tile_geo(rows, cols, grid, words_for(m));
+    if (which == 4) geo = tile_geo(rows, cols, grid, words_for(m), occ4);
     if (getenv("GZ_DEBUG_PROGRESS")) {
         static unsigned *prog = nullptr;
         if (!prog) CK(cudaHostAlloc((void **)&prog, 65536 * sizeof(unsigned), cudaHostAllocMapped));
@@ -965,7 +973,7 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
     void *args4[] = {&p, &bb, &a3, &geo, &bar};
     if (which == 4) {
         if (geo.ntiles < grid) grid = geo.ntiles;   // every CTA owns at least one tile
-        geo = tile_geo(rows, cols, grid, words_for(m));
+        geo = tile_geo(rows, cols, grid, words_for(m), occ4);
         CK(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(threads), args4, dyn_smem, s));
     } else {
         CK(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(256), which == 1 ? args1 : args2, 0, s));
@@ -1151,7 +1159,7 @@ int gz_solve_pairs(const uint8_t *left, const uint8_t *right, int32_t batch, int
     const int which = choose_solver(m, sched);
     // Concurrent solves: up to `conc` pairs run at once, each a cooperative launch
     // over 1/conc of the SMs on its own stream with its own workspace slice.
-    int conc = 2;
+    int conc = 4;
     if (const char *cs = getenv("GZ_PAIR_CONC")) conc = atoi(cs);
     if (conc > 8) conc = 8;
     if ((size_t)conc * one > workspace_bytes) conc = (int)(workspace_bytes / one);

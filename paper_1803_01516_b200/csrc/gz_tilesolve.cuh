@@ -33,11 +33,14 @@ using gz3::Arr3;
 using gz3::FULL;
 
 constexpr int BLOCK = 512;   // threads per CTA (one CTA per SM)
-constexpr int SPT1 = 4;      // BFS region sites per thread at one word per site
-constexpr int REGMAX = SPT1 * BLOCK;   // BFS region words per tile (tile + halo, x words per site)
-constexpr size_t SMEM_BYTES = (size_t)(2 + 13) * REGMAX * sizeof(uint32_t);   // frontier x2 + arc masks
-// region sites per tile for NW words per site
-__host__ __device__ constexpr int region_sites(int nw) { return REGMAX / nw; }
+// BFS region words per tile (tile + halo, x words per site): 4 per thread with
+// one CTA per SM, 3 per thread with two (the shared-memory budget per CTA)
+__host__ __device__ constexpr int regmax(int occ) { return (occ == 1 ? 4 : 3) * BLOCK; }
+__host__ __device__ constexpr size_t smem_bytes(int occ) { return (size_t)(2 + 13) * regmax(occ) * sizeof(uint32_t); }
+// region sites per tile for NW words per site (a multiple of BLOCK)
+__host__ __device__ constexpr int region_sites(int nw, int occ) {
+    return (regmax(occ) / nw) / BLOCK * BLOCK > 0 ? (regmax(occ) / nw) / BLOCK * BLOCK : BLOCK;
+}
 
 struct Geo {
     int TY, TX, ny, nx, ntiles, H;
@@ -108,11 +111,11 @@ __device__ __forceinline__ void for_tile_groups(const Prob &p, const TileBox &tb
 // words per site live in shared memory; they are loaded when load_masks is set
 // -- once per sweep when every CTA owns one tile.  Word w of region site i is
 // at [w * RS + i] (RS = region_sites(NW)).
-template <int LPT, int NW, bool WIN>
+template <int LPT, int NW, bool WIN, int OCC>
 __device__ unsigned bfs_round(const Prob &p, const Arr3 &a, const Bits2 &b, const Geo &g, const TileBox &tb,
                               const uint32_t *Fin, uint32_t *Fout, const uint32_t *Vin, uint32_t *Vout, int d,
                               uint32_t *sF0, uint32_t *sF1, uint32_t *sM, bool load_masks) {
-    constexpr int RS = region_sites(NW), SPT = RS / BLOCK;
+    constexpr int RS = region_sites(NW, OCC), SPT = RS / BLOCK;
     const int P = p.P, H = g.H;
     const int ry0 = max(tb.y0 - H, 0), ry1 = min(tb.y1 + H, p.Y);
     const int rx0 = max(tb.x0 - H, 0), rx1 = min(tb.x1 + H, p.G);
@@ -224,8 +227,8 @@ __device__ unsigned bfs_round(const Prob &p, const Arr3 &a, const Bits2 &b, cons
 // ---------------------------------------------------------------------------
 // The solver.  LP = 16: two sites per warp group (m <= 16); LP = 32: one
 // (segment, site) per warp group, R segments per chain (m <= 32 R).
-template <int LP, int R, bool WIN>
-__global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b, Arr3 a, Geo g, unsigned long long *bar) {
+template <int LP, int R, bool WIN, int OCC>
+__global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 b, Arr3 a, Geo g, unsigned long long *bar) {
     constexpr int NW = R, LPT = LP * R;
     __shared__ unsigned s_f3[3], s_r3[3], s_qn[2];
     __shared__ int s_q[BLOCK];   // per-round pool of active groups (<= 32 per warp)
@@ -235,7 +238,7 @@ __global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b,
     int qround = 0;
     __syncthreads();
     int phase = 0;
-    constexpr int RS = region_sites(NW);
+    constexpr int RS = region_sites(NW, OCC);
     uint32_t *sF0 = s_dyn, *sF1 = s_dyn + NW * RS, *sM = s_dyn + 2 * NW * RS;
     const bool resident = g.ntiles <= (int)gridDim.x;   // one tile per CTA: masks stay in smem for the sweep
     const Team tm{bar, (int)gridDim.x, (int)blockIdx.x};
@@ -336,7 +339,7 @@ __global__ void __launch_bounds__(BLOCK, 1) gz_tilesolve_kernel(Prob p, Bits2 b,
             unsigned flags = 0;
             FOR_TILES {
                 const TileBox tb(p, g, tile);
-                flags |= bfs_round<LPT, NW, WIN>(p, a, b, g, tb, Fin, Fout, Vin, Vout, d, sF0, sF1, sM,
+                flags |= bfs_round<LPT, NW, WIN, OCC>(p, a, b, g, tb, Fin, Fout, Vin, Vout, d, sF0, sF1, sM,
                                                  d == 0 || !resident);
             }
             const unsigned gf = TEAM_OR(flags);
