@@ -6,8 +6,9 @@ mkdir -p gpurun_out
 nvidia-smi > gpurun_out/nvsmi_$tag.txt 2>&1
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu_$tag.log 2>&1; echo "pytest rc $?" >> gpurun_out/pytest_gpu_$tag.log
 timeout 600 python bench.py > gpurun_out/bench_$tag.json 2> gpurun_out/bench_$tag.err; echo "bench rc $?" >> gpurun_out/bench_$tag.err
+timeout 300 python bench.py --impl reference --steps 1 --warmup 1 > gpurun_out/bench_ref_$tag.json 2> gpurun_out/bench_ref_$tag.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$tag.csv \
-    python bench.py --steps 2 --warmup 3 --pairs 4 --no-cpu-baseline > gpurun_out/ncu_launch_$tag.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:gz_warpsolve -s 3 -c 1 \
-    -o gpurun_out/prof_$tag -f python bench.py --steps 1 --warmup 3 --pairs 1 --no-cpu-baseline > gpurun_out/ncu_full_$tag.log 2>&1
+    python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch_$tag.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:gz_tilesolve -s 48 -c 1 \
+    -o gpurun_out/prof_$tag -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full_$tag.log 2>&1
 echo done
