@@ -913,7 +913,9 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
     // default BFS depth before a global relabel may stop at the first excess, and
     // (exact v4 solves) pulses per sweep: both scale with the chain length m
     // (measured: C1 m=16 best at 48 / 12, C2 m=60 at 128 / 48; tools/sweep_cfg.py)
-    if (!v1 && p.bfs_cap == 0) p.bfs_cap = which == 4 ? (2 * m + 16 > 48 ? 2 * m + 16 : 48) : 64;
+    // (m > 64: the early stop starves far excess; exhaustive relabels converge in
+    // ~60x fewer sweeps at 960x540x128, tools/sweep_cfg.py C3q)
+    if (!v1 && p.bfs_cap == 0) p.bfs_cap = which == 4 ? (m > 64 ? -1 : (2 * m + 16 > 48 ? 2 * m + 16 : 48)) : 64;
     if (which == 4 && !p.capped && m - 12 > p.K) p.K = m - 12;
     if (which == 4 && !p.capped) {   // tail sweeps: few active chains, pulses are cheap next to a global relabel
         const char *kt = getenv("GZ_KTAIL"), *ta = getenv("GZ_TAIL_AFTER");

@@ -42,3 +42,23 @@ def test_c3_data_term_matches_reference(gz):
     vol = gz.sad_volume_device(sc.left, sc.right, cub)
     assert list(vol.shape) == g["shape"]
     assert sha(vol.cpu().numpy().astype(np.int64)) == g["volume"]
+
+
+def test_c3_exact_certificate(gz, oracle):
+    """C3 has no reference solve (the reference's int32 CSR cannot hold its 3.6 G
+    arcs), so parity is by certificate: the device flow equals the energy of the
+    extracted labeling, recomputed here on the CPU by the pinned oracle
+    (energy.py:129-155).  A feasible flow of value F and a cut of cost F prove
+    both optimal (weak duality)."""
+    g = BIG["c3_volume"]
+    seed, w, h, dmin, dmax, m = g["args"]
+    sc = gz.make_scene(seed, w, h, dmin, dmax)
+    cub = gz.cuboid_from_disparity_range(w, h, dmin, dmax, num_labels=m)
+    vol = gz.sad_volume_device(sc.left, sc.right, cub)
+    r = gz.solve_exact(vol, gz.EnergyParams(14, 1023))
+    assert r.stats["converged"] and r.stats["const_offset"] == 0
+    lab = r.labeling
+    assert lab.shape == (h, w - dmin - 2) and lab.min() >= 0 and lab.max() < m
+    e_cpu = oracle.total_energy(lab, vol.cpu().numpy().astype(np.int64), 14, 1023)
+    assert r.flow == r.energy == e_cpu
+    print("C3 flow", r.flow, "device_ms", r.stats["device_ms"], "sweeps", r.stats["sweeps"])

@@ -6,7 +6,8 @@ import numpy as np, torch
 import paper_1803_01516_b200 as gz
 from _solve import run
 cfgs = {"C1": (384, 288, 10, 28, 16), "C2": (450, 375, 11, 59, 60), "C3": (1920, 1080, 11, 255, 128),
-        "C24": (384, 288, 10, 28, 24)}
+        "C24": (384, 288, 10, 28, 24), "C3q": (960, 540, 11, 255, 128), "C3e": (480, 270, 11, 255, 128),
+        "C1m128": (384, 288, 10, 28, 128), "C3m32": (1920, 1080, 11, 255, 32)}
 name = sys.argv[1]
 w, h, dmin, dmax, m = cfgs[name]
 Hs = [int(x) for x in sys.argv[2].split(",")]
