@@ -44,6 +44,14 @@ __device__ __forceinline__ int from_above(int v) { return __shfl_down_sync(FULL,
 template <int LP>
 __device__ __forceinline__ int from_below(int v) { return __shfl_up_sync(FULL, v, 1, LP); }     // lane j-1
 
+// c / G for 0 <= c < P (< 2^26): float reciprocal estimate, corrected by one step
+__device__ __forceinline__ int div_g(const Prob &p, int c) {
+    int y = __float2int_rz((float)c * p.inv_g);
+    if (y * p.G > c) --y;
+    else if ((y + 1) * p.G <= c) ++y;
+    return y;
+}
+
 // Per-lane context: node (t, c) plus neighbour sites.
 template <int LP, int R, bool WIN>
 struct Lane {
@@ -61,7 +69,7 @@ struct Lane {
         t = s * LP + j + 1;
         valid = lane / LP < nsites && c < p.P;
         const int cc = valid ? c : 0;
-        y = cc / p.G;
+        y = div_g(p, cc);
         g = cc - y * p.G;
         has[0] = valid && g + 1 < p.G; nc[0] = cc + 1;
         has[1] = valid && g > 0;       nc[1] = cc - 1;
@@ -103,6 +111,18 @@ __device__ __forceinline__ int dn_of(const Lane<LP, R, WIN> &L, int v, const int
     if (L.bot_edge()) r = arr[idx - 1];
     return r;
 }
+
+// Shared-memory worklist of the single-CTA tail mode (gz_tilesolve.cuh): the
+// groups a pulse leaves active and every group it pushes into.
+struct TailQ {
+    int *q;
+    unsigned *n;
+    int cap;
+    __device__ __forceinline__ void push(int grp) const {
+        const unsigned k = atomicAdd(n, 1u);
+        if ((int)k < cap) q[k] = grp;
+    }
+};
 
 // Residuals of the 14 arcs of a lane's node, target heights and kinds.
 // All shuffles are executed by every lane (uniform control flow).
@@ -310,7 +330,8 @@ __device__ void w_build(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
 // one pulse on a warp group of chains
 template <int LP, int R, bool WIN>
 __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base, int nsites, int seg, int parity,
-                        long long &flow, long long &pushes, long long &relabels, uint32_t *dirty) {
+                        long long &flow, long long &pushes, long long &relabels, uint32_t *dirty,
+                        const TailQ *tq = nullptr) {
     Lane<LP, R, WIN> L;
     L.init(p, c_base, nsites, seg);
     const int I = L.I, P = p.P;
@@ -348,6 +369,7 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
             } else if (L.top_edge()) {   // into the next segment's first node
                 atomicAdd(&ein_cur[I + 1], x_out);
                 atomicOr(&IN_cur[L.wi + P], 1u);
+                if (tq) tq->push(L.wi + P);
             }
         }
     }
@@ -382,6 +404,7 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
         lateral_target<LP, R, WIN>(L, jj, site, pos);
         atomicAdd(&ein_cur[site * LPT + pos - 1], d);
         atomicOr(&IN_cur[((pos - 1) / LP) * P + site], 1u << ((pos - 1) % LP));
+        if (tq) tq->push(LP == 16 ? site >> 1 : ((pos - 1) / LP) * P + site);
     }
     // chain-down pushes arrive at lane j-1 (adds to its excess and to its chain-up
     // residual); out of a segment's first lane they cross into the segment below
@@ -395,6 +418,7 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
         atomicAdd(&a.cu[I - 1], dn);
         atomicAdd(&ein_cur[I - 1], dn);
         atomicOr(&IN_cur[L.wi - P], 1u << (LP - 1));
+        if (tq) tq->push(L.wi - P);
     }
     // relabel a live node that could not push
     int hnew = hu;
@@ -426,6 +450,8 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
     }
     const uint32_t newA = seg_ballot<LP>(L.real && e > 0 && hnew < HINF);
     if (L.valid && L.j == 0) b.A[L.wi] = newA;
+    if (tq && __any_sync(FULL, newA != 0u) && (threadIdx.x & 31) == 0)
+        tq->push(LP == 16 ? c_base >> 1 : L.wi);
     // a push changes this site's residuals and the pair state / excess of its
     // neighbours: all their segments need their arc masks rebuilt next sweep
     const uint32_t pm = seg_ballot<LP>(pushed);

@@ -53,10 +53,12 @@ enum Kind : int { K_SRC = 0, K_REAL = 1, K_SNK = 2 };
 struct Prob {
     int Y, G, M, L;      // L = M-1 chain positions carry nodes
     int P;               // Y*G
+    float inv_g;         // 1 / G (fast site-row division, gz_chain.cuh:div_g)
     int pen, inh, hard;
     int hcap;            // stand-in capacity of uncuttable inhibit arcs (hard mode)
     int K;               // pulses per sweep
     int k_tail, tail_after;   // v4: pulses per sweep from sweep `tail_after` on (0 = K)
+    int tail_mode;            // v4: hand nearly empty pulse phases to one CTA
     int bfs_cap;         // lateral relaxations per non-final global relabel (0 = exact)
     int max_sweeps;      // honoured when capped
     int capped;
@@ -79,6 +81,7 @@ enum Ctr : int {
     CTR_ACT0 = 20,      // 3 rotating active counters
     CTR_T0 = 24,        // 6 phase timers (ns): init, mask build, bfs, pulses, reach, tail
     CTR_TRACE = 35,     // debug trace accumulator (GZ_TRACE=2)
+    CTR_TQN = 36,       // tail-mode global worklist length
     CTR_UPDATES = 30,   // node updates performed by pulses (v4)
     CTR_BAR0 = 32,      // 3 rotating team-barrier words (v4)
     CTR_COUNT = 40

@@ -876,6 +876,7 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
     Prob p;
     memset(&p, 0, sizeof(p));
     p.Y = rows; p.G = cols; p.M = m; p.L = m - 1; p.P = rows * cols;
+    p.inv_g = 1.0f / (float)cols;
     p.pen = en->penalty; p.inh = en->inhibit; p.hard = en->hard_inhibit ? 1 : 0;
     p.hcap = hcap;
     p.K = sc && sc->rounds_per_sweep > 0 ? sc->rounds_per_sweep : 12;
@@ -885,7 +886,9 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
     p.capped = sc ? ((sc->flags & GZ_SCHED_CAPPED) != 0) : 0;
     {
         const char *wd = getenv("GZ_WATCHDOG_MS");
-        p.watchdog_ns = (unsigned long long)(wd ? atof(wd) : 20000.0) * 1000000ull;
+        // default: 20 s plus 1 s per 2 M graph nodes (C3, 261 M nodes: ~150 s)
+        const double def_ms = 20000.0 + (double)rows * cols * (m - 1) / 2000.0;
+        p.watchdog_ns = (unsigned long long)(wd ? atof(wd) : def_ms) * 1000000ull;
     }
     p.trace = getenv("GZ_TRACE") ? atoi(getenv("GZ_TRACE")) : 0;
     static unsigned long long *tbuf = nullptr;
@@ -922,6 +925,8 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
         // measured (tools/tail_knobs.py, C1 seeds 0-7; C2): 96 pulses from the fifth sweep on
         p.k_tail = kt ? atoi(kt) : (p.K > 96 ? p.K : 96);
         p.tail_after = ta ? atoi(ta) : 4;
+        const char *tmode = getenv("GZ_TAIL_MODE");
+        p.tail_mode = tmode ? atoi(tmode) : 1;
     }
     if (!v1 && p.bfs_cap < 0) p.bfs_cap = 0;            // exhaustive BFS every sweep
     const void *kern = nullptr;

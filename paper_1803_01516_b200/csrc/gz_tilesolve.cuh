@@ -33,6 +33,8 @@ using gz3::Arr3;
 using gz3::FULL;
 
 constexpr int BLOCK = 512;   // threads per CTA (one CTA per SM)
+constexpr int TAIL_CTAS = 16;        // tail mode: at most this many CTAs had work in the last pulse,
+constexpr int TAIL_CTA_GROUPS = 8;   // none of them more than this many groups
 // BFS region words per tile (tile + halo, x words per site): 4 per thread with
 // one CTA per SM, 3 per thread with two (the shared-memory budget per CTA)
 __host__ __device__ constexpr int regmax(int occ) { return (occ == 1 ? 4 : 3) * BLOCK; }
@@ -56,7 +58,8 @@ struct Geo {
 struct Team {
     unsigned long long *bar;   // 3 rotating words of this team
     int nb, rank;
-    __device__ __forceinline__ unsigned sync_or(unsigned flags, int &phase, unsigned *s_f3, unsigned *s_r3) const {
+    // returns the number of CTAs that raised flag 0 (bits 0-15) and flag 1 (16-31)
+    __device__ __forceinline__ unsigned sync_count(unsigned flags, int &phase, unsigned *s_f3, unsigned *s_r3) const {
         const int k3 = phase % 3;
         const unsigned w = __reduce_or_sync(FULL, flags);
         if ((threadIdx.x & 31) == 0 && w) atomicOr(&s_f3[k3], w);
@@ -75,12 +78,16 @@ struct Team {
             } while (((old ^ cur) & 0x80000000ull) == 0ull);
             if (rank == 0) bar[(k3 + 2) % 3] = 0ull;
             __threadfence();
-            s_r3[k3] = ((cur >> 32) & 0xffffull ? 1u : 0u) | ((cur >> 48) ? 2u : 0u);
+            s_r3[k3] = (unsigned)(cur >> 32);   // CTAs with flag 0 (low 16) / flag 1 (high 16)
         }
         __syncthreads();
         const unsigned r = s_r3[k3];
         ++phase;
         return r;
+    }
+    __device__ __forceinline__ unsigned sync_or(unsigned flags, int &phase, unsigned *s_f3, unsigned *s_r3) const {
+        const unsigned c = sync_count(flags, phase, s_f3, s_r3);
+        return ((c & 0xffffu) ? 1u : 0u) | ((c >> 16) ? 2u : 0u);
     }
 };
 
@@ -232,6 +239,7 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
     constexpr int NW = R, LPT = LP * R;
     __shared__ unsigned s_f3[3], s_r3[3], s_qn[2];
     __shared__ int s_q[BLOCK];   // per-round pool of active groups (<= 32 per warp)
+    __shared__ unsigned s_tn[2];  // tail-mode worklist lengths
     extern __shared__ uint32_t s_dyn[];
     if (threadIdx.x < 3) { s_f3[threadIdx.x] = 0u; s_r3[threadIdx.x] = 0u; }
     if (threadIdx.x < 2) s_qn[threadIdx.x] = 0u;
@@ -244,6 +252,7 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
     const Team tm{bar, (int)gridDim.x, (int)blockIdx.x};
 #define TEAM_SYNC() (void)tm.sync_or(0u, phase, s_f3, s_r3)
 #define TEAM_OR(f) tm.sync_or((f), phase, s_f3, s_r3)
+#define TEAM_COUNT(f) tm.sync_count((f), phase, s_f3, s_r3)
     unsigned long long t_prev = 0, t_acc[6] = {0, 0, 0, 0, 0, 0};
     const bool timer = blockIdx.x == 0 && threadIdx.x == 0;
     if (timer) t_prev = gz2::gtimer();
@@ -260,6 +269,10 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
     const int gnw = tm.nb * nwarps, gwid = tm.rank * nwarps + warp;
     const int giter = (ngroups + gnw - 1) / gnw;
     const int ttid = tm.rank * blockDim.x + threadIdx.x, tstride = tm.nb * blockDim.x;
+    // tail mode: claim bitmap + two worklists in the (then idle) BFS shared memory
+    const int tail_bw = (ngroups + 31) / 32;
+    const int tail_cap = min(4096, ((int)(smem_bytes(OCC) / 4) - tail_bw) / 2);
+    const bool tail_ok = tail_cap >= 256 && p.tail_mode;
     long long updates = 0;   // groups processed by pulses (x CPW x LP nodes)
 
     // Scan the warps' interleaved groups (group it0+lane of every warp, 32 per
@@ -267,7 +280,7 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
     // and deal the pool round-robin to the CTA's warps: the critical path of a
     // phase is the busiest warp, and pooling per CTA flattens the Poisson spread
     // of active groups across warps.  Two pool counters alternate by round.
-#define FOR_ACTIVE_GROUPS(W1, W2, CNT, FN)                                                         \
+#define FOR_ACTIVE_GROUPS(W1, W2, CNT, CTAN, FN)                                                         \
     for (int it0 = 0; it0 < giter; it0 += 32, ++qround) {                                        \
         const int it_ = it0 + lane;                                                              \
         const int grp_ = gwid + it_ * gnw;                                                       \
@@ -287,6 +300,7 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
         __syncthreads();                                                                         \
         if (threadIdx.x == 0) s_qn[(qround + 1) & 1] = 0u;                                       \
         const int n_ = (int)*qn_;                                                                \
+        CTAN += n_;                                                                              \
         for (int q_ = warp; q_ < n_; q_ += nwarps) {                                             \
             const int gg_ = s_q[q_];                                                             \
             const int cb_ = LP == 16 ? 2 * gg_ : gg_ % p.P, sg_ = LP == 16 ? 0 : gg_ / p.P;      \
@@ -308,6 +322,9 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
     const int bfs_min = p.bfs_cap > 0 ? p.bfs_cap : (1 << 30);
     for (;;) {
         // ---- sweep set-up: bulk coalesced resets, then arc masks of dirty sites only ----
+        // (every inbox is merged by the builds below, so the inbox parity restarts)
+        parity = 0;
+        if (threadIdx.x == 0 && tm.rank == 0) p.ctr[CTR_TQN] = 0ull;
         for (int w = ttid; w < nwords; w += tstride) {
             const int c = w % p.P, s = w / p.P;
             const int hi = WIN ? p.hi[c] : p.L;
@@ -322,12 +339,13 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
         }
         {
             long long dummy = 0;
+            int dummy2 = 0;
             auto build = [&](int cb, int sg) {
                 gz3::w_build<LP, R, WIN>(p, a, b, cb, CPW, sg);
                 const int w0 = sg * p.P + cb;
                 if (lane < CPW && cb + lane < p.P) b.IN[w0 + lane] = 0u;
             };
-            FOR_ACTIVE_GROUPS(b.IN, b.IN, dummy, build)
+            FOR_ACTIVE_GROUPS(b.IN, b.IN, dummy, dummy2, build)
         }
         TEAM_SYNC();
         TICK(1);
@@ -371,10 +389,13 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
                 gz3::w_pulse<LP, R, WIN>(p, a, b, cb, CPW, sg, parity, flow, pushes, relabels, b.IN);
             };
             long long upd0 = updates;
-            FOR_ACTIVE_GROUPS(b.A, IN_prev, updates, pulse_fn)
+            int cta_groups = 0;
+            FOR_ACTIVE_GROUPS(b.A, IN_prev, updates, cta_groups, pulse_fn)
             if (p.trace > 1 && lane == 0 && updates != upd0) atomicAdd(&p.ctr[CTR_TRACE], (unsigned long long)(updates - upd0));
-            // an empty pulse (no active or inbox word anywhere) ends the sweep early
-            const bool idle = TEAM_OR(updates != upd0 ? 1u : 0u) == 0u;
+            // an empty pulse (no active or inbox word anywhere) ends the sweep early;
+            // a nearly empty one hands the rest of the sweep to CTA 0 (tail mode)
+            const unsigned cnt = TEAM_COUNT((cta_groups > 0 ? 1u : 0u) | (cta_groups > TAIL_CTA_GROUPS ? 2u : 0u));
+            const bool idle = (cnt & 0xffffu) == 0u;
             if (p.trace > 1 && p.tbuf && threadIdx.x == 0 && tm.rank == 0 && pulses < 4096) {
                 const unsigned long long now = gz2::gtimer();
                 p.tbuf[2 * pulses] = ((unsigned long long)sweeps << 48) | ((unsigned long long)pulse << 32) |
@@ -386,6 +407,69 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
             parity ^= 1;
             ++pulses;
             if (idle) break;
+            if (tail_ok && sweeps >= p.tail_after && pulse + 1 < kp && (cnt >> 16) == 0u &&
+                (cnt & 0xffffu) <= TAIL_CTAS) {
+                // ---- tail mode: the few active groups go to CTA 0, which runs the rest of
+                // the sweep's pulses on a shared-memory worklist with CTA barriers only ----
+                const uint32_t *INn = parity ? a.IN0 : a.IN1;
+                unsigned *gq_n = (unsigned *)&p.ctr[CTR_TQN];
+                int *gq = (int *)b.F1;   // BFS frontier buffer, idle during pulses
+                for (int it0 = 0; it0 < giter; it0 += 32) {
+                    const int it_ = it0 + lane, grp_ = gwid + it_ * gnw;
+                    uint32_t wk_ = 0u;
+                    if (it_ < giter && grp_ < ngroups) {
+                        const int w0_ = LP == 16 ? 2 * grp_ : grp_;
+                        wk_ = b.A[w0_] | INn[w0_];
+                        if (LP == 16 && w0_ + 1 < p.P) wk_ |= b.A[w0_ + 1] | INn[w0_ + 1];
+                    }
+                    const uint32_t msk_ = __ballot_sync(FULL, wk_ != 0u);
+                    int base_ = 0;
+                    if (lane == 0 && msk_) base_ = (int)atomicAdd(gq_n, (unsigned)__popc(msk_));
+                    base_ = __shfl_sync(FULL, base_, 0);
+                    if ((msk_ >> lane) & 1u) gq[base_ + __popc(msk_ & ((1u << lane) - 1u))] = grp_;
+                }
+                TEAM_SYNC();
+                if (tm.rank == 0) {
+                    uint32_t *bits = s_dyn;                       // claim bitmap over groups
+                    int *qa = (int *)(s_dyn + tail_bw), *qb = qa + tail_cap;
+                    const int n0 = (int)*(volatile unsigned *)gq_n;
+                    if (n0 <= tail_cap) {
+                        for (int w = threadIdx.x; w < tail_bw; w += blockDim.x) bits[w] = 0u;
+                        for (int q = threadIdx.x; q < n0; q += blockDim.x) qa[q] = gq[q];
+                        if (threadIdx.x == 0) { s_tn[0] = (unsigned)n0; s_tn[1] = 0u; }
+                        __syncthreads();
+                        int cur = 0;
+                        for (int tp = pulse + 1; tp < kp; ++tp) {
+                            const int n = (int)min(s_tn[cur], (unsigned)tail_cap);
+                            if (n == 0) break;
+                            int *ql = cur ? qb : qa;
+                            const gz3::TailQ tq{cur ? qa : qb, &s_tn[cur ^ 1], tail_cap};
+                            for (int q = warp; q < n; q += nwarps) {
+                                const int gg = ql[q];
+                                unsigned old = 0u;
+                                if (lane == 0) old = atomicOr(&bits[gg >> 5], 1u << (gg & 31));
+                                old = __shfl_sync(FULL, old, 0);
+                                if ((old >> (gg & 31)) & 1u) continue;   // already processed this pulse
+                                const int cb = LP == 16 ? 2 * gg : gg % p.P, sg = LP == 16 ? 0 : gg / p.P;
+                                gz3::w_pulse<LP, R, WIN>(p, a, b, cb, CPW, sg, parity, flow, pushes, relabels, b.IN, &tq);
+                                ++updates;
+                            }
+                            __syncthreads();
+                            for (int q = threadIdx.x; q < n; q += blockDim.x) bits[ql[q] >> 5] = 0u;
+                            const bool ovf = s_tn[cur ^ 1] > (unsigned)tail_cap;
+                            __syncthreads();
+                            if (threadIdx.x == 0) s_tn[cur] = 0u;
+                            parity ^= 1;
+                            ++pulses;
+                            cur ^= 1;
+                            __syncthreads();
+                            if (ovf) break;   // worklist overflow: the A / inbox words hold the rest
+                        }
+                    }
+                }
+                TEAM_SYNC();
+                break;
+            }
         }
         TICK(3);
         ++sweeps;
@@ -437,6 +521,7 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
 #undef FOR_TILES
 #undef TEAM_SYNC
 #undef TEAM_OR
+#undef TEAM_COUNT
     TICK(5);
 #undef TICK
     if (timer)
