@@ -174,6 +174,27 @@ struct Arcs {
 
         const int t = L.t, P2 = 2 * p.pen, cap = p.hard ? p.hcap : p.inh;
         const bool top_ok = t < p.L;   // a position t+1 <= L exists (diagonals up)
+        if (!WIN) {
+            // full windows: for a real node (1 <= t <= L) the only terminal targets are
+            // the sink above t = L (chain up) and the source below t = 1 (chain down and
+            // inhibit diagonals down); every lateral target is a real node
+            const bool bot = t == 1, top = t == p.L;
+            kd[A_UP] = top ? K_SNK : K_REAL; r[A_UP] = w_cu; hv[A_UP] = top ? 0 : h_above;
+            kd[A_DN] = bot ? K_SRC : K_REAL; r[A_DN] = bot ? 0 : HINF; hv[A_DN] = h_below;
+            kd[A_SR] = K_REAL; r[A_SR] = L.has[0] ? w_ph : 0; hv[A_SR] = hn[0];
+            kd[A_SL] = K_REAL; r[A_SL] = L.has[1] ? P2 - w_phL : 0; hv[A_SL] = hn[1];
+            kd[A_SD] = K_REAL; r[A_SD] = L.has[2] ? w_pv : 0; hv[A_SD] = hn[2];
+            kd[A_SU] = K_REAL; r[A_SU] = L.has[3] ? P2 - w_pvU : 0; hv[A_SU] = hn[3];
+            kd[A_UR] = K_REAL; r[A_UR] = (L.has[0] && top_ok) ? w_dbr_up : 0; hv[A_UR] = hn_above[0];
+            kd[A_UL] = K_REAL; r[A_UL] = (L.has[1] && top_ok) ? w_darL_up : 0; hv[A_UL] = hn_above[1];
+            kd[A_UD] = K_REAL; r[A_UD] = (L.has[2] && top_ok) ? w_dbd_up : 0; hv[A_UD] = hn_above[2];
+            kd[A_UU] = K_REAL; r[A_UU] = (L.has[3] && top_ok) ? w_dadU_up : 0; hv[A_UU] = hn_above[3];
+            kd[A_DR] = bot ? K_SRC : K_REAL; r[A_DR] = (L.has[0] && !bot) ? cap - w_dar : 0; hv[A_DR] = hn_below[0];
+            kd[A_DL] = bot ? K_SRC : K_REAL; r[A_DL] = (L.has[1] && !bot) ? cap - w_dbrL : 0; hv[A_DL] = hn_below[1];
+            kd[A_DD] = bot ? K_SRC : K_REAL; r[A_DD] = (L.has[2] && !bot) ? cap - w_dad : 0; hv[A_DD] = hn_below[2];
+            kd[A_DU] = bot ? K_SRC : K_REAL; r[A_DU] = (L.has[3] && !bot) ? cap - w_dbdU : 0; hv[A_DU] = hn_below[3];
+            return;
+        }
 #define SETA(J, RR, KIND, HV) do { kd[J] = (KIND); r[J] = (KIND) == K_SRC ? 0 : (RR); hv[J] = (KIND) == K_SNK ? 0 : (HV); } while (0)
         SETA(A_UP, w_cu, L.kown(t + 1), h_above);
         SETA(A_DN, HINF, L.kown(t - 1), h_below);
