@@ -97,18 +97,23 @@ struct Lane {
     __device__ __forceinline__ bool bot_edge() const { return R > 1 && j == 0 && s > 0 && valid; }
 };
 
+// global load of solver state; CG = bypass L1 (the asynchronous pulses: other
+// SMs and this warp's own atomics update the state between two reads)
+template <bool CG>
+__device__ __forceinline__ int ldx(const int32_t *p) { return CG ? __ldcg(p) : *p; }
+
 // value at position t+1 / t-1 of the same array: shuffle inside the segment,
 // load across a segment boundary (every lane executes the shuffle)
-template <int LP, int R, bool WIN>
+template <bool CG = false, int LP, int R, bool WIN>
 __device__ __forceinline__ int up_of(const Lane<LP, R, WIN> &L, int v, const int32_t *arr, int idx, bool ok = true) {
     int r = from_above<LP>(v);
-    if (ok && L.top_edge()) r = arr[idx + 1];
+    if (ok && L.top_edge()) r = ldx<CG>(arr + idx + 1);
     return r;
 }
-template <int LP, int R, bool WIN>
+template <bool CG = false, int LP, int R, bool WIN>
 __device__ __forceinline__ int dn_of(const Lane<LP, R, WIN> &L, int v, const int32_t *arr, int idx) {
     int r = from_below<LP>(v);
-    if (L.bot_edge()) r = arr[idx - 1];
+    if (L.bot_edge()) r = ldx<CG>(arr + idx - 1);
     return r;
 }
 
@@ -126,7 +131,7 @@ struct TailQ {
 
 // Residuals of the 14 arcs of a lane's node, target heights and kinds.
 // All shuffles are executed by every lane (uniform control flow).
-template <int LP, int R, bool WIN>
+template <int LP, int R, bool WIN, bool CG = false>
 struct Arcs {
     int r[A_COUNT], hv[A_COUNT], kd[A_COUNT];
     // raw words (for write-back)
@@ -138,38 +143,38 @@ struct Arcs {
     __device__ __forceinline__ void load(const Prob &p, const Arr3 &a, const Lane<LP, R, WIN> &L) {
         const int I = L.I;
         const bool v = L.valid;
-        w_cu = v ? a.cu[I] : 0;
-        w_ph = v ? a.ph[I] : 0;
-        w_pv = v ? a.pv[I] : 0;
-        w_dar = v ? a.dar[I] : 0;
-        w_dbr = v ? a.dbr[I] : 0;
-        w_dad = v ? a.dad[I] : 0;
-        w_dbd = v ? a.dbd[I] : 0;
+        w_cu = v ? ldx<CG>(a.cu + I) : 0;
+        w_ph = v ? ldx<CG>(a.ph + I) : 0;
+        w_pv = v ? ldx<CG>(a.pv + I) : 0;
+        w_dar = v ? ldx<CG>(a.dar + I) : 0;
+        w_dbr = v ? ldx<CG>(a.dbr + I) : 0;
+        w_dad = v ? ldx<CG>(a.dad + I) : 0;
+        w_dbd = v ? ldx<CG>(a.dbd + I) : 0;
         const int iL = L.nidx(1), iU = L.nidx(3);
-        w_phL = L.has[1] ? a.ph[iL] : 0;
-        w_darL = L.has[1] ? a.dar[iL] : 0;
-        w_dbrL = L.has[1] ? a.dbr[iL] : 0;
-        w_pvU = L.has[3] ? a.pv[iU] : 0;
-        w_dadU = L.has[3] ? a.dad[iU] : 0;
-        w_dbdU = L.has[3] ? a.dbd[iU] : 0;
+        w_phL = L.has[1] ? ldx<CG>(a.ph + iL) : 0;
+        w_darL = L.has[1] ? ldx<CG>(a.dar + iL) : 0;
+        w_dbrL = L.has[1] ? ldx<CG>(a.dbr + iL) : 0;
+        w_pvU = L.has[3] ? ldx<CG>(a.pv + iU) : 0;
+        w_dadU = L.has[3] ? ldx<CG>(a.dad + iU) : 0;
+        w_dbdU = L.has[3] ? ldx<CG>(a.dbd + iU) : 0;
         int hn[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) hn[i] = L.has[i] ? a.h[L.nidx(i)] : HINF;
-        h_u = v ? a.h[I] : HINF;
+        for (int i = 0; i < 4; ++i) hn[i] = L.has[i] ? ldx<CG>(a.h + L.nidx(i)) : HINF;
+        h_u = v ? ldx<CG>(a.h + I) : HINF;
         // position t+1 / t-1 values
-        w_dbr_up = up_of(L, w_dbr, a.dbr, I);
-        w_darL_up = up_of(L, w_darL, a.dar, iL, L.has[1]);
-        w_dbd_up = up_of(L, w_dbd, a.dbd, I);
-        w_dadU_up = up_of(L, w_dadU, a.dad, iU, L.has[3]);
-        const int h_above = up_of(L, h_u, a.h, I), h_below = dn_of(L, h_u, a.h, I);
+        w_dbr_up = up_of<CG>(L, w_dbr, a.dbr, I);
+        w_darL_up = up_of<CG>(L, w_darL, a.dar, iL, L.has[1]);
+        w_dbd_up = up_of<CG>(L, w_dbd, a.dbd, I);
+        w_dadU_up = up_of<CG>(L, w_dadU, a.dad, iU, L.has[3]);
+        const int h_above = up_of<CG>(L, h_u, a.h, I), h_below = dn_of<CG>(L, h_u, a.h, I);
         int hn_above[4], hn_below[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int ni = L.has[i] ? L.nidx(i) : 0;
             hn_above[i] = from_above<LP>(hn[i]);
             hn_below[i] = from_below<LP>(hn[i]);
-            if (L.top_edge() && L.has[i]) hn_above[i] = a.h[ni + 1];
-            if (L.bot_edge() && L.has[i]) hn_below[i] = a.h[ni - 1];
+            if (L.top_edge() && L.has[i]) hn_above[i] = ldx<CG>(a.h + ni + 1);
+            if (L.bot_edge() && L.has[i]) hn_below[i] = ldx<CG>(a.h + ni - 1);
         }
 
         const int t = L.t, P2 = 2 * p.pen, cap = p.hard ? p.hcap : p.inh;
@@ -327,10 +332,14 @@ __device__ void w_build(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
     const int x0 = L.valid ? a.ein0[I] : 0, x1 = L.valid ? a.ein1[I] : 0;
     Arcs<LP, R, WIN> A;
     A.load(p, a, L);
-    // merge both inbox buffers (the last pulse's lateral pushes)
-    if ((in0 >> L.j) & 1u) { e += x0; a.ein0[I] = 0; }
-    if ((in1 >> L.j) & 1u) { e += x1; a.ein1[I] = 0; }
-    if (L.valid && ((in0 | in1) >> L.j) & 1u) a.e[I] = e;
+    // merge both inbox buffers (pushes since the last merge).  Values are merged
+    // whether or not their inbox bit is set: an asynchronous pulse can consume a
+    // bit before the value it announces lands (gz_tilesolve.cuh, async pulses),
+    // and the pusher always marks this site dirty, so it is merged here.
+    (void)in0; (void)in1;
+    if (x0) { e += x0; a.ein0[I] = 0; }
+    if (x1) { e += x1; a.ein1[I] = 0; }
+    if (L.valid && (x0 | x1)) a.e[I] = e;
     uint32_t m[13];
 #pragma unroll
     for (int q = 0; q < 13; ++q) m[q] = seg_ballot<LP>(L.real && A.r[q] > 0);
@@ -349,7 +358,7 @@ __device__ void w_build(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
 
 // ---------------------------------------------------------------------------
 // one pulse on a warp group of chains
-template <int LP, int R, bool WIN>
+template <int LP, int R, bool WIN, bool ASYNC = false>
 __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base, int nsites, int seg, int parity,
                         long long &flow, long long &pushes, long long &relabels, uint32_t *dirty,
                         const TailQ *tq = nullptr) {
@@ -357,19 +366,32 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
     L.init(p, c_base, nsites, seg);
     const int I = L.I, P = p.P;
     constexpr int LPT = Lane<LP, R, WIN>::LPT;
-    uint32_t *IN_prev = parity ? a.IN0 : a.IN1;
-    uint32_t *IN_cur = parity ? a.IN1 : a.IN0;
-    int32_t *ein_prev = parity ? a.ein0 : a.ein1;
-    int32_t *ein_cur = parity ? a.ein1 : a.ein0;
-    // all loads before the first store: one round trip per group (ein_prev has
-    // no writer during this pulse, so reading it unconditionally is safe)
-    const uint32_t inb = L.valid ? IN_prev[L.wi] : 0u;
-    int e = L.valid ? a.e[I] : 0;
-    const int xin = L.valid ? ein_prev[I] : 0;
-    Arcs<LP, R, WIN> A;
-    A.load(p, a, L);
-    if ((inb >> L.j) & 1u) { e += xin; ein_prev[I] = 0; }
-    if (L.valid && L.j == 0 && inb) IN_prev[L.wi] = 0u;
+    // synchronous pulses double-buffer the inbox by parity; asynchronous ones use
+    // one buffer consumed atomically
+    uint32_t *IN_prev = (ASYNC || parity) ? a.IN0 : a.IN1;
+    uint32_t *IN_cur = (ASYNC || !parity) ? a.IN0 : a.IN1;
+    int32_t *ein_prev = (ASYNC || parity) ? a.ein0 : a.ein1;
+    int32_t *ein_cur = (ASYNC || !parity) ? a.ein0 : a.ein1;
+    int e, xin;
+    Arcs<LP, R, WIN, ASYNC> A;
+    if (ASYNC) {
+        uint32_t inb = 0u;
+        if (L.valid && L.j == 0) inb = atomicExch(&IN_prev[L.wi], 0u);
+        e = L.valid ? __ldcg(a.e + I) : 0;
+        xin = L.valid ? atomicExch(&ein_prev[I], 0) : 0;
+        A.load(p, a, L);
+        (void)__shfl_sync(FULL, inb, (threadIdx.x & 31) & ~(LP - 1));
+        e += xin;
+    } else {
+        // all loads before the first store: one round trip per group (ein_prev has
+        // no writer during this pulse, so reading it unconditionally is safe)
+        const uint32_t inb = L.valid ? IN_prev[L.wi] : 0u;
+        e = L.valid ? a.e[I] : 0;
+        xin = L.valid ? ein_prev[I] : 0;
+        A.load(p, a, L);
+        if ((inb >> L.j) & 1u) { e += xin; ein_prev[I] = 0; }
+        if (L.valid && L.j == 0 && inb) IN_prev[L.wi] = 0u;
+    }
     const int hu = A.h_u;
     const bool live = L.real && hu < HINF;
     // upward chain wave through admissible chain arcs
@@ -436,7 +458,7 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
         cu_new += dn_in;
     }
     if (dn > 0 && L.bot_edge()) {
-        atomicAdd(&a.cu[I - 1], dn);
+        atomicAdd(&a.cu[I - 1], dn);   // (the segment below applies its own cu change atomically too)
         atomicAdd(&ein_cur[I - 1], dn);
         atomicOr(&IN_cur[L.wi - P], 1u << (LP - 1));
         if (tq) tq->push(L.wi - P);
@@ -452,7 +474,26 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
         ++relabels;
     }
     // write back
-    if (L.real) {
+    if (ASYNC && L.real) {
+        // pair states (and the chain residual, which a segment above can change)
+        // as atomic deltas: concurrent opposite pushes on one arc pair stay within
+        // its capacity because each push is bounded by its own (stale-low) read
+        a.e[I] = e;
+        if (cu_new != A.w_cu) atomicAdd(&a.cu[I], cu_new - A.w_cu);
+        if (hnew != hu) a.h[I] = hnew;
+        if (ph_d) atomicAdd(&a.ph[I], ph_d);
+        if (pv_d) atomicAdd(&a.pv[I], pv_d);
+        if (dar_d) atomicAdd(&a.dar[I], dar_d);
+        if (dad_d) atomicAdd(&a.dad[I], dad_d);
+        if (phL_d) atomicAdd(&a.ph[L.nidx(1)], phL_d);
+        if (dbrL_d) atomicAdd(&a.dbr[L.nidx(1)], dbrL_d);
+        if (pvU_d) atomicAdd(&a.pv[L.nidx(3)], pvU_d);
+        if (dbdU_d) atomicAdd(&a.dbd[L.nidx(3)], dbdU_d);
+        if (dbr_up_d) atomicAdd(&a.dbr[I + 1], dbr_up_d);
+        if (dbd_up_d) atomicAdd(&a.dbd[I + 1], dbd_up_d);
+        if (darL_up_d) atomicAdd(&a.dar[L.nidx(1) + 1], darL_up_d);
+        if (dadU_up_d) atomicAdd(&a.dad[L.nidx(3) + 1], dadU_up_d);
+    } else if (L.real) {
         a.e[I] = e;
         if (cu_new != A.w_cu) a.cu[I] = cu_new;
         if (hnew != hu) a.h[I] = hnew;

@@ -927,6 +927,8 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
         p.tail_after = ta ? atoi(ta) : 4;
         const char *tmode = getenv("GZ_TAIL_MODE");
         p.tail_mode = tmode ? atoi(tmode) : 1;
+        const char *al = getenv("GZ_ASYNC_L");
+        p.async_l = al ? atoi(al) : 0;
     }
     if (!v1 && p.bfs_cap < 0) p.bfs_cap = 0;            // exhaustive BFS every sweep
     const void *kern = nullptr;

@@ -287,8 +287,8 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
         uint32_t wk_ = 0u;                                                                       \
         if (it_ < giter && grp_ < ngroups) {                                                     \
             const int w0_ = LP == 16 ? 2 * grp_ : grp_;                                          \
-            wk_ = (W1)[w0_] | (W2)[w0_];                                                         \
-            if (LP == 16 && w0_ + 1 < p.P) wk_ |= (W1)[w0_ + 1] | (W2)[w0_ + 1];                 \
+            wk_ = __ldcg((W1) + w0_) | __ldcg((W2) + w0_);                                       \
+            if (LP == 16 && w0_ + 1 < p.P) wk_ |= __ldcg((W1) + w0_ + 1) | __ldcg((W2) + w0_ + 1); \
         }                                                                                        \
         const uint32_t msk_ = __ballot_sync(FULL, wk_ != 0u);                                    \
         CNT += __popc(msk_);                                                                     \
@@ -390,7 +390,18 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
             };
             long long upd0 = updates;
             int cta_groups = 0;
-            FOR_ACTIVE_GROUPS(b.A, IN_prev, updates, cta_groups, pulse_fn)
+            if (p.async_l > 0) {
+                // asynchronous pulse: async_l scan-and-process iterations per team
+                // barrier; pushes between warps are picked up within the pulse
+                auto pulse_async = [&](int cb, int sg) {
+                    gz3::w_pulse<LP, R, WIN, true>(p, a, b, cb, CPW, sg, 0, flow, pushes, relabels, b.IN);
+                };
+                for (int ai = 0; ai < p.async_l; ++ai) {
+                    FOR_ACTIVE_GROUPS(b.A, a.IN0, updates, cta_groups, pulse_async)
+                }
+            } else {
+                FOR_ACTIVE_GROUPS(b.A, IN_prev, updates, cta_groups, pulse_fn)
+            }
             if (p.trace > 1 && lane == 0 && updates != upd0) atomicAdd(&p.ctr[CTR_TRACE], (unsigned long long)(updates - upd0));
             // an empty pulse (no active or inbox word anywhere) ends the sweep early;
             // a nearly empty one hands the rest of the sweep to CTA 0 (tail mode)
@@ -407,7 +418,7 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
             parity ^= 1;
             ++pulses;
             if (idle) break;
-            if (tail_ok && sweeps >= p.tail_after && pulse + 1 < kp && (cnt >> 16) == 0u &&
+            if (tail_ok && p.async_l == 0 && sweeps >= p.tail_after && pulse + 1 < kp && (cnt >> 16) == 0u &&
                 (cnt & 0xffffu) <= TAIL_CTAS) {
                 // ---- tail mode: the few active groups go to CTA 0, which runs the rest of
                 // the sweep's pulses on a shared-memory worklist with CTA barriers only ----
