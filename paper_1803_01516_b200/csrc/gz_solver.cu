@@ -920,6 +920,11 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
     // ~60x fewer sweeps at 960x540x128, tools/sweep_cfg.py C3q)
     if (!v1 && p.bfs_cap == 0) p.bfs_cap = which == 4 ? (m > 64 ? -1 : (2 * m + 16 > 48 ? 2 * m + 16 : 48)) : 64;
     if (which == 4 && !p.capped && m - 12 > p.K) p.K = m - 12;
+    // capped (level-2) solves: a reference sweep discharges every active node 12
+    // times (FIFO rounds, maxflow.py:183-250); a synchronous pulse moves excess one
+    // hop, so the GPU sweep runs 2m pulses (24-label ladder: converges inside the
+    // 8-sweep cap at b=3, tools/l2_quality.py)
+    if (p.capped && 2 * m > p.K) p.K = 2 * m;
     if (which == 4 && !p.capped) {   // tail sweeps: few active chains, pulses are cheap next to a global relabel
         const char *kt = getenv("GZ_KTAIL"), *ta = getenv("GZ_TAIL_AFTER");
         // measured (tools/tail_knobs.py, C1 seeds 0-7; C2): 96 pulses from the fifth sweep on

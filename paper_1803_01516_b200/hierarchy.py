@@ -97,7 +97,8 @@ def solve_level1(volume, params: EnergyParams, block: int, skin_radius: int = DE
     result.stats.update(
         level=1, block=block, skin_radius=skin_radius, coarse_energy=coarse.energy,
         coarse_wall_s=coarse.stats["wall_s"], mean_window=float((hi - lo + 1).double().mean()),
-        wall_s=time.perf_counter() - t0)
+        coarse_device_ms=coarse.stats["device_ms"],
+        device_ms_total=coarse.stats["device_ms"] + result.stats["device_ms"], wall_s=time.perf_counter() - t0)
     if solver == "dinic":
         result.stats["requested_solver"] = "dinic"
     return result
@@ -118,5 +119,7 @@ def solve_level2(volume, params: EnergyParams, block: int, skin_radius: int = DE
     result.stats.update(
         level=2, block=block, skin_radius=skin_radius, coarse_energy=coarse.energy,
         coarse_wall_s=coarse.stats["wall_s"], mean_window=float((hi - lo + 1).double().mean()),
+        coarse_device_ms=coarse.stats["device_ms"],
+        device_ms_total=coarse.stats["device_ms"] + result.stats["device_ms"],
         nodes=net.n_nodes, arcs=net.num_arcs, wall_s=time.perf_counter() - t0)
     return result
