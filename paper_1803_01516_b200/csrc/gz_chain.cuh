@@ -133,7 +133,8 @@ struct TailQ {
 // All shuffles are executed by every lane (uniform control flow).
 template <int LP, int R, bool WIN, bool CG = false>
 struct Arcs {
-    int r[A_COUNT], hv[A_COUNT], kd[A_COUNT];
+    int r[A_COUNT], hv[A_COUNT];
+    unsigned snk;   // bit j: arc j leads into the sink (arcs into the source have r = 0)
     // raw words (for write-back)
     int w_cu, w_ph, w_pv, w_dar, w_dbr, w_dad, w_dbd;   // own-stored at I
     int w_phL, w_pvU, w_darL, w_dbrL, w_dadU, w_dbdU;   // neighbour-stored at the same position
@@ -184,23 +185,25 @@ struct Arcs {
             // the sink above t = L (chain up) and the source below t = 1 (chain down and
             // inhibit diagonals down); every lateral target is a real node
             const bool bot = t == 1, top = t == p.L;
-            kd[A_UP] = top ? K_SNK : K_REAL; r[A_UP] = w_cu; hv[A_UP] = top ? 0 : h_above;
-            kd[A_DN] = bot ? K_SRC : K_REAL; r[A_DN] = bot ? 0 : HINF; hv[A_DN] = h_below;
-            kd[A_SR] = K_REAL; r[A_SR] = L.has[0] ? w_ph : 0; hv[A_SR] = hn[0];
-            kd[A_SL] = K_REAL; r[A_SL] = L.has[1] ? P2 - w_phL : 0; hv[A_SL] = hn[1];
-            kd[A_SD] = K_REAL; r[A_SD] = L.has[2] ? w_pv : 0; hv[A_SD] = hn[2];
-            kd[A_SU] = K_REAL; r[A_SU] = L.has[3] ? P2 - w_pvU : 0; hv[A_SU] = hn[3];
-            kd[A_UR] = K_REAL; r[A_UR] = (L.has[0] && top_ok) ? w_dbr_up : 0; hv[A_UR] = hn_above[0];
-            kd[A_UL] = K_REAL; r[A_UL] = (L.has[1] && top_ok) ? w_darL_up : 0; hv[A_UL] = hn_above[1];
-            kd[A_UD] = K_REAL; r[A_UD] = (L.has[2] && top_ok) ? w_dbd_up : 0; hv[A_UD] = hn_above[2];
-            kd[A_UU] = K_REAL; r[A_UU] = (L.has[3] && top_ok) ? w_dadU_up : 0; hv[A_UU] = hn_above[3];
-            kd[A_DR] = bot ? K_SRC : K_REAL; r[A_DR] = (L.has[0] && !bot) ? cap - w_dar : 0; hv[A_DR] = hn_below[0];
-            kd[A_DL] = bot ? K_SRC : K_REAL; r[A_DL] = (L.has[1] && !bot) ? cap - w_dbrL : 0; hv[A_DL] = hn_below[1];
-            kd[A_DD] = bot ? K_SRC : K_REAL; r[A_DD] = (L.has[2] && !bot) ? cap - w_dad : 0; hv[A_DD] = hn_below[2];
-            kd[A_DU] = bot ? K_SRC : K_REAL; r[A_DU] = (L.has[3] && !bot) ? cap - w_dbdU : 0; hv[A_DU] = hn_below[3];
+            snk = top ? 1u << A_UP : 0u;
+            r[A_UP] = w_cu; hv[A_UP] = top ? 0 : h_above;
+            r[A_DN] = bot ? 0 : HINF; hv[A_DN] = h_below;
+            r[A_SR] = L.has[0] ? w_ph : 0; hv[A_SR] = hn[0];
+            r[A_SL] = L.has[1] ? P2 - w_phL : 0; hv[A_SL] = hn[1];
+            r[A_SD] = L.has[2] ? w_pv : 0; hv[A_SD] = hn[2];
+            r[A_SU] = L.has[3] ? P2 - w_pvU : 0; hv[A_SU] = hn[3];
+            r[A_UR] = (L.has[0] && top_ok) ? w_dbr_up : 0; hv[A_UR] = hn_above[0];
+            r[A_UL] = (L.has[1] && top_ok) ? w_darL_up : 0; hv[A_UL] = hn_above[1];
+            r[A_UD] = (L.has[2] && top_ok) ? w_dbd_up : 0; hv[A_UD] = hn_above[2];
+            r[A_UU] = (L.has[3] && top_ok) ? w_dadU_up : 0; hv[A_UU] = hn_above[3];
+            r[A_DR] = (L.has[0] && !bot) ? cap - w_dar : 0; hv[A_DR] = hn_below[0];
+            r[A_DL] = (L.has[1] && !bot) ? cap - w_dbrL : 0; hv[A_DL] = hn_below[1];
+            r[A_DD] = (L.has[2] && !bot) ? cap - w_dad : 0; hv[A_DD] = hn_below[2];
+            r[A_DU] = (L.has[3] && !bot) ? cap - w_dbdU : 0; hv[A_DU] = hn_below[3];
             return;
         }
-#define SETA(J, RR, KIND, HV) do { kd[J] = (KIND); r[J] = (KIND) == K_SRC ? 0 : (RR); hv[J] = (KIND) == K_SNK ? 0 : (HV); } while (0)
+        snk = 0u;
+#define SETA(J, RR, KIND, HV) do { const int k_ = (KIND); if (k_ == K_SNK) snk |= 1u << (J); r[J] = k_ == K_SRC ? 0 : (RR); hv[J] = k_ == K_SNK ? 0 : (HV); } while (0)
         SETA(A_UP, w_cu, L.kown(t + 1), h_above);
         SETA(A_DN, HINF, L.kown(t - 1), h_below);
         SETA(A_SR, L.has[0] ? w_ph : 0, L.has[0] ? L.knb(0, t) : K_SRC, hn[0]);
@@ -395,7 +398,7 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
     const int hu = A.h_u;
     const bool live = L.real && hu < HINF;
     // upward chain wave through admissible chain arcs
-    const bool adm_up = live && A.r[A_UP] > 0 && A.kd[A_UP] != K_SRC && hu == A.hv[A_UP] + 1;
+    const bool adm_up = live && A.r[A_UP] > 0 && hu == A.hv[A_UP] + 1;
     const int x_out = chain_wave<LP>(adm_up ? A.r[A_UP] : 0, adm_up ? max(e, 0) : 0, L.j);
     const int x_below = from_below<LP>(x_out);   // every lane shuffles (full mask)
     const int x_in = L.j > 0 ? x_below : 0;
@@ -407,7 +410,7 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
             cu_new -= x_out;
             pushed = true;
             ++pushes;
-            if (A.kd[A_UP] == K_SNK) {
+            if ((A.snk >> A_UP) & 1u) {
                 flow += x_out;
             } else if (L.top_edge()) {   // into the next segment's first node
                 atomicAdd(&ein_cur[I + 1], x_out);
@@ -424,7 +427,7 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
         int rem = (live && e > 0) ? e : 0;
 #pragma unroll
         for (int jj = A_SR; jj <= A_DN; ++jj) {
-            const bool adm = A.kd[jj] != K_SRC && A.r[jj] > 0 && hu == A.hv[jj] + 1;
+            const bool adm = A.r[jj] > 0 && hu == A.hv[jj] + 1;
             const int d = adm ? min(rem, A.r[jj]) : 0;
             dd[jj] = d;
             rem -= d;
@@ -442,7 +445,7 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
         pushed = true;
         ++pushes;
         if (jj == A_DN) continue;
-        if (A.kd[jj] == K_SNK) { flow += d; continue; }
+        if ((A.snk >> jj) & 1u) { flow += d; continue; }
         int site, pos;
         lateral_target<LP, R, WIN>(L, jj, site, pos);
         atomicAdd(&ein_cur[site * LPT + pos - 1], d);
@@ -469,7 +472,7 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
         int best = HINF;
 #pragma unroll
         for (int jj = 0; jj < A_COUNT; ++jj)
-            if (A.kd[jj] != K_SRC && A.r[jj] > 0) best = min(best, A.hv[jj] + 1);
+            if (A.r[jj] > 0) best = min(best, A.hv[jj] + 1);
         hnew = best;
         ++relabels;
     }
