@@ -204,7 +204,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--pairs", type=int, default=16, help="pairs per rank per step")
+    ap.add_argument("--pairs", type=int, default=64,
+                    help="pairs per rank per step (64: N=8 ranks solve BASELINE config 4's 512-pair batch per step)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=32)
