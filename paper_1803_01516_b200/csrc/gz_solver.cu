@@ -770,7 +770,7 @@ size_t bit_bytes(int rows, int cols, int m) {
 }
 
 // positions per site row of the v4 solver's node arrays (16, or 32 x segments; 0: m too large)
-int lanes_for(int m) { return m <= 16 ? 16 : (m <= 128 ? 32 * words_for(m) : 0); }
+int lanes_for(int m) { return m <= 16 ? 16 : (m <= 256 ? 32 * words_for(m) : 0); }
 
 size_t ws_bytes(int rows, int cols, int m) {
     const int mp = m > lanes_for(m) ? m : lanes_for(m);
@@ -951,6 +951,7 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
     if (which == 4) {
 #define GZ_PICK4(LP_, R_, O_) if (LPn == LP_ * R_ && occ4 == O_) kern = win ? (const void *)gz4::gz_tilesolve_kernel<LP_, R_, true, O_> : (const void *)gz4::gz_tilesolve_kernel<LP_, R_, false, O_>;
         GZ_PICK4(16, 1, 1) GZ_PICK4(16, 1, 2) GZ_PICK4(32, 1, 1) GZ_PICK4(32, 2, 1) GZ_PICK4(32, 4, 1)
+        GZ_PICK4(32, 8, 1)
 #undef GZ_PICK4
     } else if (which == 2) {
         GZ_PICK_NW(1) GZ_PICK_NW(2) GZ_PICK_NW(4) GZ_PICK_NW(8)

@@ -39,9 +39,13 @@ constexpr int TAIL_CTA_GROUPS = 8;   // none of them more than this many groups
 // one CTA per SM, 3 per thread with two (the shared-memory budget per CTA)
 __host__ __device__ constexpr int regmax(int occ) { return (occ == 1 ? 4 : 3) * BLOCK; }
 __host__ __device__ constexpr size_t smem_bytes(int occ) { return (size_t)(2 + 13) * regmax(occ) * sizeof(uint32_t); }
+// arc masks of the BFS region live in shared memory up to 4 words per site; 8
+// words per site (m > 128) read them from global memory
+__host__ __device__ constexpr bool smem_masks(int nw) { return nw <= 4; }
 // region sites per tile for NW words per site (a multiple of BLOCK)
 __host__ __device__ constexpr int region_sites(int nw, int occ) {
-    return (regmax(occ) / nw) / BLOCK * BLOCK > 0 ? (regmax(occ) / nw) / BLOCK * BLOCK : BLOCK;
+    return smem_masks(nw) ? ((regmax(occ) / nw) / BLOCK * BLOCK > 0 ? (regmax(occ) / nw) / BLOCK * BLOCK : BLOCK)
+                          : BLOCK;
 }
 
 struct Geo {
@@ -141,7 +145,7 @@ __device__ unsigned bfs_round(const Prob &p, const Arr3 &a, const Bits2 &b, cons
         C[k] = ok ? c : -1;
         IN_[k] = ok && y >= tb.y0 && y < tb.y1 && x >= tb.x0 && x < tb.x1;
         NB[k] = (rj + 1 < RW ? 1u : 0u) | (rj > 0 ? 2u : 0u) | (i + RW < nreg ? 4u : 0u) | (ri > 0 ? 8u : 0u);
-        if (load_masks && ok) {
+        if (smem_masks(NW) && load_masks && ok) {
 #pragma unroll
             for (int q = 0; q < 13 * NW; ++q) sM[q * RS + i] = b.mask[(size_t)q * P + c];
         }
@@ -181,9 +185,11 @@ __device__ unsigned bfs_round(const Prob &p, const Arr3 &a, const Bits2 &b, cons
                 for (int w = 0; w < NW; ++w) nxt[w * RS + i] = 0u;
                 continue;
             }
+            // mask word (arc q, word w) of this site: shared memory, or global memory (NW = 8)
+#define GZ_MASK(q, w) (smem_masks(NW) ? sM[((q) * NW + (w)) * RS + i] : __ldg(b.mask + ((size_t)(q) * NW + (w)) * P + C[k]))
             BW<NW> M0;
 #pragma unroll
-            for (int w = 0; w < NW; ++w) M0.w[w] = sM[(A_UP * NW + w) * RS + i];
+            for (int w = 0; w < NW; ++w) M0.w[w] = GZ_MASK(A_UP, w);
             BW<NW> N = F.shl1() | (F.shr1() & M0);
 #pragma unroll
             for (int dir = 0; dir < 4; ++dir) {
@@ -191,12 +197,13 @@ __device__ unsigned bfs_round(const Prob &p, const Arr3 &a, const Bits2 &b, cons
                 BW<NW> ms, md, mu;
 #pragma unroll
                 for (int w = 0; w < NW; ++w) {
-                    ms.w[w] = sM[((A_SR + dir) * NW + w) * RS + i];
-                    md.w[w] = sM[((A_DR + dir) * NW + w) * RS + i];
-                    mu.w[w] = sM[((A_UR + dir) * NW + w) * RS + i];
+                    ms.w[w] = GZ_MASK(A_SR + dir, w);
+                    md.w[w] = GZ_MASK(A_DR + dir, w);
+                    mu.w[w] = GZ_MASK(A_UR + dir, w);
                 }
                 N = N | (Fn[dir] & ms) | (Fn[dir].shl1() & md) | (Fn[dir].shr1() & mu);
             }
+#undef GZ_MASK
             N = gz2::andnot(N & RNG[k], V[k]);
             V[k] = V[k] | N;
 #pragma unroll

@@ -97,3 +97,18 @@ def test_c1_level1(gz, oracle):
         want = oracle.solve_level1(vol, 14, 1023, b)
         assert r.energy == want["energy"] and np.array_equal(r.labeling, want["labeling"])
         print("C1 L1 b", b, r.energy, r.stats["device_ms"], r.stats["wall_s"])
+
+
+@pytest.mark.parametrize("m", [33, 70, 129, 200, 256])
+def test_long_chains_match_oracle(gz, oracle, m):
+    """Chains of 2-8 warp segments (m > 32): segment-crossing waves and pushes,
+    multi-word BFS (global-memory masks at m > 128), against the oracle."""
+    rng = np.random.default_rng(1000 + m)
+    for _ in range(3):
+        rows, cols = int(rng.integers(2, 6)), int(rng.integers(2, 6))
+        vol = rng.integers(0, 120, (rows, cols, m)).astype(np.int64)
+        pen, inh = int(rng.integers(1, 9)), int(rng.integers(0, 60))
+        got = gz.solve_exact(vol, gz.EnergyParams(pen, inh))
+        want = oracle.solve_exact(vol, pen, inh)
+        assert got.flow == want["flow"] and got.energy == want["energy"]
+        assert np.array_equal(got.labeling, want["labeling"])
