@@ -62,3 +62,19 @@ def test_c3_exact_certificate(gz, oracle):
     e_cpu = oracle.total_energy(lab, vol.cpu().numpy().astype(np.int64), 14, 1023)
     assert r.flow == r.energy == e_cpu
     print("C3 flow", r.flow, "device_ms", r.stats["device_ms"], "sweeps", r.stats["sweeps"])
+
+
+def test_c5_data_term_matches_reference(gz):
+    """C5 (3840x2160, 256 labels): the device data term equals the reference's
+    sad_volume (digest from oracle/make_golden_c5.py); hashed in row chunks so
+    host memory stays small."""
+    g = BIG["c5_volume"]
+    seed, w, h, dmin, dmax, m = g["args"]
+    sc = gz.make_scene(seed, w, h, dmin, dmax)
+    cub = gz.cuboid_from_disparity_range(w, h, dmin, dmax, num_labels=m)
+    vol = gz.sad_volume_device(sc.left, sc.right, cub)
+    assert list(vol.shape) == g["shape"]
+    hs = hashlib.sha256()
+    for r0 in range(0, vol.shape[0], 64):
+        hs.update(np.ascontiguousarray(vol[r0:r0 + 64].cpu().numpy().astype(np.int64)).tobytes())
+    assert hs.hexdigest() == g["volume"]
