@@ -103,7 +103,10 @@ int gz_solve_volume(const int32_t *vol, int32_t rows, int32_t cols, int32_t m, c
 /* Fused path: sad_volume + solve_exact for `batch` stereo pairs laid out
  * back to back (left/right: batch x height x width x channels uint8).
  * labels_out: batch x (y_extent, g_extent) int32; stats_out: batch entries
- * (host memory).  workspace: batch * gz_workspace_bytes(y_extent, g_extent, m). */
+ * (host memory).  workspace: k * gz_workspace_bytes(y_extent, g_extent, m)
+ * runs up to k pair solves at once (k <= 4 by default, env GZ_PAIR_CONC), each
+ * a cooperative launch over 1/k of the SMs on its own stream; at least one
+ * workspace is required. */
 int gz_solve_pairs(const uint8_t *left, const uint8_t *right, int32_t batch, int32_t img_h, int32_t img_w,
                    int32_t channels, const gz_cuboid *cuboid, const gz_energy *energy, const gz_sched *sched,
                    int32_t *labels_out, gz_stats *stats_out, void *workspace, size_t workspace_bytes,
@@ -127,6 +130,17 @@ int gz_coarsen(const int32_t *vol, int32_t rows, int32_t cols, int32_t m, int32_
 /* hierarchy.py:60-73 thin_skin: coarse labeling (crows, ccols) -> lo/hi (rows, cols). */
 int gz_thin_skin(const int32_t *coarse_labels, int32_t crows, int32_t ccols, int32_t rows, int32_t cols,
                  int32_t m, int32_t block, int32_t radius, int32_t *lo_out, int32_t *hi_out, void *stream);
+
+/* Runtime knobs (environment, read per solve; defaults are the measured best):
+ *   GZ_PAIR_CONC     concurrent pair solves in gz_solve_pairs (4)
+ *   GZ_OCC           2: occupancy-2 instance for m <= 16 (default when concurrent)
+ *   GZ_BFS_H         BFS levels per temporally blocked round (8)
+ *   GZ_KTAIL, GZ_TAIL_AFTER   pulses per sweep from sweep GZ_TAIL_AFTER on (max(K, 96), 4)
+ *   GZ_TAIL_MODE     0 disables the single-CTA tail mode (1)
+ *   GZ_ASYNC_L       > 0: asynchronous pulses, iterations per team barrier (0)
+ *   GZ_WATCHDOG_MS   device watchdog (20 s + 1 s per 2 M nodes)
+ *   GZ_TRACE         1: per-sweep device trace, 2: per-pulse trace to stderr
+ */
 
 /* Human-readable status. */
 const char *gz_status_string(int status);
