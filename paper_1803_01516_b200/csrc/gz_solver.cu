@@ -919,6 +919,10 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
     // (m > 64: the early stop starves far excess; exhaustive relabels converge in
     // ~60x fewer sweeps at 960x540x128, tools/sweep_cfg.py C3q)
     if (!v1 && p.bfs_cap == 0) p.bfs_cap = which == 4 ? (m > 64 ? -1 : (2 * m + 16 > 48 ? 2 * m + 16 : 48)) : 64;
+    if (which == 4 && !p.capped) {   // tuning overrides (GZ_K pulses per sweep, GZ_BFS_CAP)
+        if (const char *k = getenv("GZ_K")) p.K = atoi(k) > 0 ? atoi(k) : p.K;
+        if (const char *bc = getenv("GZ_BFS_CAP")) p.bfs_cap = atoi(bc);
+    }
     if (which == 4 && !p.capped && m - 12 > p.K) p.K = m - 12;
     // capped (level-2) solves: a reference sweep discharges every active node 12
     // times (FIFO rounds, maxflow.py:183-250); a synchronous pulse moves excess one
