@@ -766,7 +766,8 @@ int words_for(int m) {
 size_t bit_bytes(int rows, int cols, int m) {
     const size_t P = (size_t)rows * cols;
     const int NW = words_for(m) ? words_for(m) : 1;
-    return align_up((size_t)(13 + 9) * NW * P * 4) + 2 * align_up(P * 4);
+    // + R0 (P ints) and R1 (2P ints: also the BFS per-tile flag pair, ntiles <= P)
+    return align_up((size_t)(13 + 9) * NW * P * 4) + align_up(P * 4) + align_up(2 * P * 4);
 }
 
 // positions per site row of the v4 solver's node arrays (16, or 32 x segments; 0: m too large)

@@ -125,7 +125,7 @@ __device__ __forceinline__ void for_tile_groups(const Prob &p, const TileBox &tb
 template <int LPT, int NW, bool WIN, int OCC>
 __device__ unsigned bfs_round(const Prob &p, const Arr3 &a, const Bits2 &b, const Geo &g, const TileBox &tb,
                               const uint32_t *Fin, uint32_t *Fout, const uint32_t *Vin, uint32_t *Vout, int d,
-                              uint32_t *sF0, uint32_t *sF1, uint32_t *sM, bool load_masks) {
+                              uint32_t *sF0, uint32_t *sF1, uint32_t *sM, bool load_masks, bool &front) {
     constexpr int RS = region_sites(NW, OCC), SPT = RS / BLOCK;
     const int P = p.P, H = g.H;
     const int ry0 = max(tb.y0 - H, 0), ry1 = min(tb.y1 + H, p.Y);
@@ -226,15 +226,20 @@ __device__ unsigned bfs_round(const Prob &p, const Arr3 &a, const Bits2 &b, cons
         __syncthreads();
         uint32_t *t = cur; cur = nxt; nxt = t;
     }
+    bool fr = false;
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
         if (!IN_[k]) continue;
         const int i = threadIdx.x + k * blockDim.x;
 #pragma unroll
-        for (int w = 0; w < NW; ++w) Fout[(size_t)w * P + C[k]] = cur[w * RS + i];
+        for (int w = 0; w < NW; ++w) {
+            const uint32_t f = cur[w * RS + i];
+            fr |= f != 0u;
+            Fout[(size_t)w * P + C[k]] = f;
+        }
         V[k].store(Vout, P, C[k]);
     }
-    __syncthreads();   // shared buffers are reused by the next tile
+    front = __syncthreads_or(fr) != 0;   // also: shared buffers are reused by the next tile
     return flags;
 }
 
@@ -360,17 +365,44 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
         int d = 0;
         bool found = false, exhausted = false;
         uint32_t *Fin = b.F0, *Fout = b.F1, *Vin = b.V, *Vout = b.RL;
+        // per-tile "interior frontier nonempty" flags of the last round (reach arrays
+        // are idle during the BFS); a tile whose neighbourhood within H sites had no
+        // frontier cannot gain nodes this round and only carries its words forward
+        int32_t *tf_in = b.R1, *tf_out = b.R1 + g.ntiles;
+        const int rty = (g.H + g.TY - 1) / g.TY, rtx = (g.H + g.TX - 1) / g.TX;
         for (;;) {
             unsigned flags = 0;
             FOR_TILES {
                 const TileBox tb(p, g, tile);
-                flags |= bfs_round<LPT, NW, WIN, OCC>(p, a, b, g, tb, Fin, Fout, Vin, Vout, d, sF0, sF1, sM,
-                                                 d == 0 || !resident);
+                bool act = d == 0;
+                if (!act) {
+                    const int ty = tile / g.nx, tx = tile - ty * g.nx;
+                    for (int dy = -rty; dy <= rty && !act; ++dy)
+                        for (int dx = -rtx; dx <= rtx && !act; ++dx) {
+                            const int yy = ty + dy, xx = tx + dx;
+                            if (yy >= 0 && yy < g.ny && xx >= 0 && xx < g.nx) act = __ldcg(tf_in + yy * g.nx + xx) != 0;
+                        }
+                }
+                bool front = false;
+                if (act) {
+                    flags |= bfs_round<LPT, NW, WIN, OCC>(p, a, b, g, tb, Fin, Fout, Vin, Vout, d, sF0, sF1, sM,
+                                                         d == 0 || !resident, front);
+                } else {
+                    for (int r = tb.y0 + warp; r < tb.y1; r += nwarps)
+                        for (int x = tb.x0 + lane; x < tb.x1; x += 32)
+                            for (int w = 0; w < NW; ++w) {
+                                const size_t q = (size_t)w * p.P + r * p.G + x;
+                                Fout[q] = 0u;
+                                Vout[q] = Vin[q];
+                            }
+                }
+                if (threadIdx.x == 0) tf_out[tile] = front ? 1 : 0;
             }
             const unsigned gf = TEAM_OR(flags);
             found |= (gf & 2u) != 0;
             uint32_t *t = Fin; Fin = Fout; Fout = t;
             t = Vin; Vin = Vout; Vout = t;
+            int32_t *tt = tf_in; tf_in = tf_out; tf_out = tt;
             d += g.H;
             if (!(gf & 1u)) { exhausted = true; break; }
             if (found && d >= bfs_min) break;
