@@ -104,7 +104,7 @@ int gz_solve_volume(const int32_t *vol, int32_t rows, int32_t cols, int32_t m, c
  * back to back (left/right: batch x height x width x channels uint8).
  * labels_out: batch x (y_extent, g_extent) int32; stats_out: batch entries
  * (host memory).  workspace: k * gz_workspace_bytes(y_extent, g_extent, m)
- * runs up to k pair solves at once (k <= 4 by default, env GZ_PAIR_CONC), each
+ * runs up to k pair solves at once (k <= 8, env GZ_PAIR_CONC), each
  * a cooperative launch over 1/k of the SMs on its own stream; at least one
  * workspace is required. */
 int gz_solve_pairs(const uint8_t *left, const uint8_t *right, int32_t batch, int32_t img_h, int32_t img_w,
@@ -132,7 +132,7 @@ int gz_thin_skin(const int32_t *coarse_labels, int32_t crows, int32_t ccols, int
                  int32_t m, int32_t block, int32_t radius, int32_t *lo_out, int32_t *hi_out, void *stream);
 
 /* Runtime knobs (environment, read per solve; defaults are the measured best):
- *   GZ_PAIR_CONC     concurrent pair solves in gz_solve_pairs (4)
+ *   GZ_PAIR_CONC     concurrent pair solves in gz_solve_pairs (8)
  *   GZ_OCC           2: occupancy-2 instance for m <= 16 (default when concurrent)
  *   GZ_BFS_H         BFS levels per temporally blocked round (8)
  *   GZ_KTAIL, GZ_TAIL_AFTER   pulses per sweep from sweep GZ_TAIL_AFTER on (max(K, 96), 4)
