@@ -60,6 +60,7 @@ struct Prob {
     int k_tail, tail_after;   // v4: pulses per sweep from sweep `tail_after` on (0 = K)
     int tail_mode;            // v4: hand nearly empty pulse phases to one CTA
     int async_l;              // v4: > 0 = asynchronous pulses, this many iterations per team barrier
+    int bfs_adapt;            // v4: double the BFS early-stop depth when excess lies only beyond it
     int bfs_cap;         // lateral relaxations per non-final global relabel (0 = exact)
     int max_sweeps;      // honoured when capped
     int capped;

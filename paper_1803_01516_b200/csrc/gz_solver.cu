@@ -917,9 +917,12 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
     // default BFS depth before a global relabel may stop at the first excess, and
     // (exact v4 solves) pulses per sweep: both scale with the chain length m
     // (measured: C1 m=16 best at 48 / 12, C2 m=60 at 128 / 48; tools/sweep_cfg.py)
-    // (m > 64: the early stop starves far excess; exhaustive relabels converge in
-    // ~60x fewer sweeps at 960x540x128, tools/sweep_cfg.py C3q)
-    if (!v1 && p.bfs_cap == 0) p.bfs_cap = which == 4 ? (m > 64 ? -1 : (2 * m + 16 > 48 ? 2 * m + 16 : 48)) : 64;
+    // m > 64: a fixed early-stop depth starves far excess (at 960x540x128, 2m+16
+    // levels -> 1600 sweeps, 3m -> 32); start at 3m and double it whenever a relabel
+    // meets excess only beyond it (tools/sweep_cfg.py C3q / C3)
+    if (!v1 && p.bfs_cap == 0) p.bfs_cap = which == 4 ? (m > 64 ? 3 * m : (2 * m + 16 > 48 ? 2 * m + 16 : 48)) : 64;
+    p.bfs_adapt = (which == 4 && m > 64) ? 1 : 0;
+    if (const char *ba = getenv("GZ_BFS_ADAPT")) p.bfs_adapt = atoi(ba);
     if (which == 4 && !p.capped) {   // tuning overrides (GZ_K pulses per sweep, GZ_BFS_CAP)
         if (const char *k = getenv("GZ_K")) p.K = atoi(k) > 0 ? atoi(k) : p.K;
         if (const char *bc = getenv("GZ_BFS_CAP")) p.bfs_cap = atoi(bc);

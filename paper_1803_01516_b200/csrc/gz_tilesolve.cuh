@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
     int sweeps = 0, levels_total = 0, pulses = 0, parity = 0;
     int converged = 1;
     bool err = false;
-    const int bfs_min = p.bfs_cap > 0 ? p.bfs_cap : (1 << 30);
+    int bfs_min = p.bfs_cap > 0 ? p.bfs_cap : (1 << 30);
     for (;;) {
         // ---- sweep set-up: bulk coalesced resets, then arc masks of dirty sites only ----
         // (every inbox is merged by the builds below, so the inbox parity restarts)
@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
         TEAM_SYNC();
         TICK(1);
         // ---- global relabel: temporally blocked BFS ----
-        int d = 0;
+        int d = 0, d_found = 0;
         bool found = false, exhausted = false;
         uint32_t *Fin = b.F0, *Fout = b.F1, *Vin = b.V, *Vout = b.RL;
         // per-tile "interior frontier nonempty" flags of the last round (reach arrays
@@ -399,6 +399,7 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
                 if (threadIdx.x == 0) tf_out[tile] = front ? 1 : 0;
             }
             const unsigned gf = TEAM_OR(flags);
+            if (!found && (gf & 2u)) d_found = d + g.H;
             found |= (gf & 2u) != 0;
             uint32_t *t = Fin; Fin = Fout; Fout = t;
             t = Vin; Vin = Vout; Vout = t;
@@ -409,6 +410,9 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
             if (d > 4 * (p.P + p.M) + 4 * g.H) { if (threadIdx.x == 0 && tm.rank == 0) vctr[CTR_STATUS] = (unsigned long long)(-GZ_ERR_NOCONVERGE); err = true; break; }
         }
         levels_total += d;
+        // adaptive depth (p.bfs_adapt): excess met only beyond the current early-stop
+        // depth means the near region is drained -- double the depth
+        if (p.bfs_adapt && found && d_found > bfs_min && bfs_min < (1 << 29)) bfs_min *= 2;
         TICK(2);
         if (err) break;
         if (!found && exhausted) break;
