@@ -914,20 +914,22 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
     const bool det = p.capped != 0;
     const int which = choose_solver(m, sc);
     const bool v1 = which == 1;
-    // default BFS depth before a global relabel may stop at the first excess, and
-    // (exact v4 solves) pulses per sweep: both scale with the chain length m
-    // (measured: C1 m=16 best at 48 / 12, C2 m=60 at 128 / 48; tools/sweep_cfg.py)
-    // m > 64: a fixed early-stop depth starves far excess (at 960x540x128, 2m+16
-    // levels -> 1600 sweeps, 3m -> 32); start at 3m and double it whenever a relabel
-    // meets excess only beyond it (tools/sweep_cfg.py C3q / C3)
-    if (!v1 && p.bfs_cap == 0) p.bfs_cap = which == 4 ? (m > 64 ? 3 * m : (2 * m + 16 > 48 ? 2 * m + 16 : 48)) : 64;
-    p.bfs_adapt = (which == 4 && m > 64) ? 1 : 0;
+    // Exact v4 solves stop a relabel early once it is max(24, m) levels deep and has
+    // met excess, and double that depth whenever a relabel meets excess only beyond
+    // it (the near region is drained).  A fixed depth either wastes levels (C1/C2)
+    // or starves far excess (960x540x128: 2m+16 levels -> 1600 sweeps); adaptive:
+    // C1 ~420 -> ~490 pairs/s, C2 88 -> 58 ms, C3 30 -> 12 s (tools/bench_tune.py,
+    // tools/sweep_cfg.py)
+    if (!v1 && p.bfs_cap == 0) p.bfs_cap = which == 4 ? (m > 24 ? m : 24) : 64;
+    p.bfs_adapt = (which == 4 && !p.capped) ? 1 : 0;
     if (const char *ba = getenv("GZ_BFS_ADAPT")) p.bfs_adapt = atoi(ba);
+    // exact v4 solves (canonical cut: the schedule only affects speed) use their own
+    // tuned pulses per sweep instead of the reference's rounds_per_sweep
+    if (which == 4 && !p.capped) p.K = m - 12 > 8 ? m - 12 : 8;
     if (which == 4 && !p.capped) {   // tuning overrides (GZ_K pulses per sweep, GZ_BFS_CAP)
         if (const char *k = getenv("GZ_K")) p.K = atoi(k) > 0 ? atoi(k) : p.K;
         if (const char *bc = getenv("GZ_BFS_CAP")) p.bfs_cap = atoi(bc);
     }
-    if (which == 4 && !p.capped && m - 12 > p.K) p.K = m - 12;
     // capped (level-2) solves: a reference sweep discharges every active node 12
     // times (FIFO rounds, maxflow.py:183-250); a synchronous pulse moves excess one
     // hop, so the GPU sweep runs 2m pulses (24-label ladder: converges inside the
@@ -935,8 +937,8 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
     if (p.capped && 2 * m > p.K) p.K = 2 * m;
     if (which == 4 && !p.capped) {   // tail sweeps: few active chains, pulses are cheap next to a global relabel
         const char *kt = getenv("GZ_KTAIL"), *ta = getenv("GZ_TAIL_AFTER");
-        // measured (tools/tail_knobs.py, C1 seeds 0-7; C2): 96 pulses from the fifth sweep on
-        p.k_tail = kt ? atoi(kt) : (p.K > 96 ? p.K : 96);
+        // measured (tools/bench_tune.py with adaptive relabels): 64 pulses from the fifth sweep on
+        p.k_tail = kt ? atoi(kt) : (p.K > 64 ? p.K : 64);
         p.tail_after = ta ? atoi(ta) : 4;
         const char *tmode = getenv("GZ_TAIL_MODE");
         p.tail_mode = tmode ? atoi(tmode) : 1;
