@@ -361,7 +361,7 @@ __device__ void w_build(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
 
 // ---------------------------------------------------------------------------
 // one pulse on a warp group of chains
-template <int LP, int R, bool WIN, bool ASYNC = false>
+template <int LP, int R, bool WIN, bool ASYNC = false, bool DETPUSH = false>
 __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base, int nsites, int seg, int parity,
                         long long &flow, long long &pushes, long long &relabels, uint32_t *dirty,
                         const TailQ *tq = nullptr) {
@@ -372,12 +372,17 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
     // synchronous pulses double-buffer the inbox by parity; asynchronous ones use
     // one buffer consumed atomically
     uint32_t *IN_prev = (ASYNC || parity) ? a.IN0 : a.IN1;
-    uint32_t *IN_cur = (ASYNC || !parity) ? a.IN0 : a.IN1;
+    uint32_t *IN_cur = (ASYNC || DETPUSH || !parity) ? a.IN0 : a.IN1;
     int32_t *ein_prev = (ASYNC || parity) ? a.ein0 : a.ein1;
-    int32_t *ein_cur = (ASYNC || !parity) ? a.ein0 : a.ein1;
+    int32_t *ein_cur = (ASYNC || DETPUSH || !parity) ? a.ein0 : a.ein1;
     int e, xin;
     Arcs<LP, R, WIN, ASYNC> A;
-    if (ASYNC) {
+    if (DETPUSH) {
+        // deterministic push phase: inboxes are merged by the commit phase
+        e = L.valid ? a.e[I] : 0;
+        xin = 0;
+        A.load(p, a, L);
+    } else if (ASYNC) {
         uint32_t inb = 0u;
         if (L.valid && L.j == 0) inb = atomicExch(&IN_prev[L.wi], 0u);
         e = L.valid ? __ldcg(a.e + I) : 0;
@@ -466,9 +471,9 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
         atomicOr(&IN_cur[L.wi - P], 1u << (LP - 1));
         if (tq) tq->push(L.wi - P);
     }
-    // relabel a live node that could not push
+    // relabel a live node that could not push (deterministic mode: a later phase)
     int hnew = hu;
-    if (live && !pushed && e > 0) {
+    if (!DETPUSH && live && !pushed && e > 0) {
         int best = HINF;
 #pragma unroll
         for (int jj = 0; jj < A_COUNT; ++jj)
@@ -513,8 +518,12 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
         if (darL_up_d) a.dar[L.nidx(1) + 1] = A.w_darL_up + darL_up_d;
         if (dadU_up_d) a.dad[L.nidx(3) + 1] = A.w_dadU_up + dadU_up_d;
     }
-    const uint32_t newA = seg_ballot<LP>(L.real && e > 0 && hnew < HINF);
+    const uint32_t newA = seg_ballot<LP>(L.real && e > 0 && hnew < HINF && (!DETPUSH || pushed));
     if (L.valid && L.j == 0) b.A[L.wi] = newA;
+    if (DETPUSH) {   // relabel candidates for the relabel phase
+        const uint32_t rl = seg_ballot<LP>(live && !pushed && e > 0);
+        if (L.valid && L.j == 0) b.RL[L.wi] = rl;
+    }
     if (tq && __any_sync(FULL, newA != 0u) && (threadIdx.x & 31) == 0)
         tq->push(LP == 16 ? c_base >> 1 : L.wi);
     // a push changes this site's residuals and the pair state / excess of its
@@ -528,6 +537,48 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
             for (int i = 0; i < 4; ++i)
                 if (L.has[i]) dirty[q * P + L.nc[i]] = 1u;
         }
+    }
+}
+
+// Deterministic relabel phase (capped solves): relabel candidates of the push
+// phase take one above their lowest residual neighbour; the state is settled
+// (no pushes run in this phase) and heights are written to h2 (commit phase).
+template <int LP, int R, bool WIN>
+__device__ void w_relabel(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base, int nsites, int seg,
+                          int32_t *h2, long long &relabels) {
+    Lane<LP, R, WIN> L;
+    L.init(p, c_base, nsites, seg);
+    const uint32_t rl = L.valid ? b.RL[L.wi] : 0u;
+    Arcs<LP, R, WIN> A;
+    A.load(p, a, L);
+    if (L.valid && ((rl >> L.j) & 1u)) {
+        int best = HINF;
+#pragma unroll
+        for (int jj = 0; jj < A_COUNT; ++jj)
+            if (A.r[jj] > 0) best = min(best, A.hv[jj] + 1);
+        h2[L.I] = best;
+        ++relabels;
+    }
+}
+
+// Deterministic commit phase: relabeled heights take effect, inboxes merge, and
+// the active bits of the touched nodes are recomputed.
+template <int LP, int R, bool WIN>
+__device__ void w_commit(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base, int nsites, int seg, int32_t *h2) {
+    Lane<LP, R, WIN> L;
+    L.init(p, c_base, nsites, seg);
+    const int I = L.I;
+    const uint32_t rl = L.valid ? b.RL[L.wi] : 0u, inb = L.valid ? a.IN0[L.wi] : 0u;
+    const bool r_ = (rl >> L.j) & 1u, i_ = (inb >> L.j) & 1u;
+    int h = L.valid ? a.h[I] : HINF, e = L.valid ? a.e[I] : 0;
+    if (r_) { h = h2[I]; a.h[I] = h; h2[I] = 0; }
+    if (i_) { e += a.ein0[I]; a.ein0[I] = 0; a.e[I] = e; }
+    const uint32_t touched = seg_ballot<LP>(r_ || i_);
+    const uint32_t act = seg_ballot<LP>((r_ || i_) && L.real && e > 0 && h < HINF);
+    if (L.valid && L.j == 0) {
+        b.A[L.wi] = (b.A[L.wi] & ~touched) | act;
+        b.RL[L.wi] = 0u;
+        a.IN0[L.wi] = 0u;
     }
 }
 

@@ -832,7 +832,8 @@ int coop_grid(const void *kernel, int threads, int *grid_out, size_t dyn_smem = 
 int choose_solver(int m, const gz_sched *sc) {
     const int flags = sc ? sc->flags : 0;
     if ((flags & GZ_SCHED_V1) || words_for(m) == 0) return 1;
-    if ((flags & GZ_SCHED_V2) || (flags & GZ_SCHED_CAPPED) || lanes_for(m) == 0) return 2;
+    if ((flags & GZ_SCHED_V2) || lanes_for(m) == 0) return 2;
+    if ((flags & GZ_SCHED_CAPPED) && getenv("GZ_CAPPED_V2")) return 2;
     return 4;
 }
 

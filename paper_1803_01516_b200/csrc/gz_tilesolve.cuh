@@ -417,7 +417,10 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
         if (err) break;
         if (!found && exhausted) break;
         if (p.capped && sweeps >= p.max_sweeps) { converged = 0; break; }
-        for (int w = ttid; w < nwords; w += tstride) b.A[w] = Vin[w] & b.EX[w];
+        for (int w = ttid; w < nwords; w += tstride) {
+            b.A[w] = Vin[w] & b.EX[w];
+            if (p.capped) b.RL[w] = 0u;   // (the BFS used RL as a visited buffer)
+        }
         TEAM_SYNC();
         unsigned long long t_pulse = p.trace > 1 ? gz2::gtimer() : 0ull;
         // pulses this sweep: K, or K_tail once the dense opening sweeps are over
@@ -433,7 +436,23 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
             };
             long long upd0 = updates;
             int cta_groups = 0;
-            if (p.async_l > 0) {
+            if (p.capped) {
+                // deterministic (capped, level-2) pulse: push | relabel into h2 | commit,
+                // each phase reading state no concurrent phase writes
+                int32_t *h2 = a.ein1;   // the second inbox plane is idle in this mode
+                auto push_fn = [&](int cb, int sg) {
+                    gz3::w_pulse<LP, R, WIN, false, true>(p, a, b, cb, CPW, sg, 0, flow, pushes, relabels, b.IN);
+                };
+                FOR_ACTIVE_GROUPS(b.A, b.A, updates, cta_groups, push_fn)
+                TEAM_SYNC();
+                long long dmy = 0;
+                int dmy2 = 0;
+                auto relabel_fn = [&](int cb, int sg) { gz3::w_relabel<LP, R, WIN>(p, a, b, cb, CPW, sg, h2, relabels); };
+                FOR_ACTIVE_GROUPS(b.RL, b.RL, dmy, dmy2, relabel_fn)
+                TEAM_SYNC();
+                auto commit_fn = [&](int cb, int sg) { gz3::w_commit<LP, R, WIN>(p, a, b, cb, CPW, sg, h2); };
+                FOR_ACTIVE_GROUPS(b.RL, a.IN0, dmy, dmy2, commit_fn)
+            } else if (p.async_l > 0) {
                 // asynchronous pulse: async_l scan-and-process iterations per team
                 // barrier; pushes between warps are picked up within the pulse
                 auto pulse_async = [&](int cb, int sg) {
@@ -461,7 +480,7 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
             parity ^= 1;
             ++pulses;
             if (idle) break;
-            if (tail_ok && p.async_l == 0 && sweeps >= p.tail_after && pulse + 1 < kp && (cnt >> 16) == 0u &&
+            if (tail_ok && p.async_l == 0 && !p.capped && sweeps >= p.tail_after && pulse + 1 < kp && (cnt >> 16) == 0u &&
                 (cnt & 0xffffu) <= TAIL_CTAS) {
                 // ---- tail mode: the few active groups go to CTA 0, which runs the rest of
                 // the sweep's pulses on a shared-memory worklist with CTA barriers only ----

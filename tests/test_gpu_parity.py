@@ -112,3 +112,25 @@ def test_long_chains_match_oracle(gz, oracle, m):
         want = oracle.solve_exact(vol, pen, inh)
         assert got.flow == want["flow"] and got.energy == want["energy"]
         assert np.array_equal(got.labeling, want["labeling"])
+
+
+@pytest.mark.parametrize("m", [6, 24, 40])
+def test_capped_solves_are_deterministic(gz, m):
+    """Capped sweeps (level 2) run the GPU's own deterministic schedule: push,
+    relabel into a second height buffer, commit.  Identical
+    flow and labeling run to run, at every sweep cap."""
+    rng = np.random.default_rng(77 + m)
+    for _ in range(3):
+        rows, cols = int(rng.integers(8, 30)), int(rng.integers(8, 30))
+        vol = rng.integers(0, 200, (rows, cols, m)).astype(np.int64)
+        p = gz.EnergyParams(int(rng.integers(1, 9)), int(rng.integers(0, 60)))
+        lo = rng.integers(0, m, rows * cols).astype(np.int32)
+        hi = np.minimum(lo + rng.integers(0, 6, rows * cols), m - 1).astype(np.int32)
+        for cap in (1, 2, 4):
+            runs = []
+            for _ in range(2):
+                net = gz.build_network(vol, p, lo, hi)
+                r = gz.maxflow_push_relabel(net, max_sweeps=cap)
+                runs.append((r.flow, r.labeling.copy(), r.stats["sweeps"], r.stats["pulses"]))
+            assert runs[0][0] == runs[1][0] and np.array_equal(runs[0][1], runs[1][1]), (m, cap)
+            assert runs[0][2:] == runs[1][2:]
