@@ -1,4 +1,4 @@
-"""Compare v3 and v4 on the golden random cases; print stats of the first mismatches."""
+"""Run the golden random cases through the default (v4) and the v2 solver; print the first mismatches."""
 import ctypes as C, json, sys
 from pathlib import Path
 ROOT = Path(__file__).resolve().parent.parent
