@@ -53,9 +53,13 @@ __device__ __forceinline__ int div_g(const Prob &p, int c) {
 }
 
 // Per-lane context: node (t, c) plus neighbour sites.
-template <int LP, int R, bool WIN>
+// RW > 0: window-relative lanes.  Lane j of a 16-lane segment handles position
+// lo + 1 + j of its site (windows of width <= 15), over the unchanged absolute
+// memory layout (rows of 32 RW positions, RW absolute bit words per site).
+template <int LP, int R, bool WIN, int RW = 0>
 struct Lane {
-    static constexpr int LPT = LP * R;
+    static constexpr int LPT = RW ? 32 * RW : LP * R;   // memory row length (positions)
+    static constexpr int NWB = RW ? RW : R;             // bit words per site
     int c, s, j, t, lo, hi, y, g, I, wi;
     bool valid, real;
     int nc[4], nlo[4], nhi[4];
@@ -85,17 +89,35 @@ struct Lane {
 #pragma unroll
             for (int i = 0; i < 4; ++i) { nlo[i] = 0; nhi[i] = p.L; }
         }
+        if (RW) {
+            t = lo + 1 + j;
+            if (t > LPT) { valid = false; t = LPT; }   // beyond the row: never real, never loaded
+        }
         real = valid && t > lo && t <= hi;
-        I = cc * LPT + t - 1;
+        I = (valid ? cc : 0) * LPT + t - 1;
         wi = s * p.P + cc;
     }
     __device__ __forceinline__ int kown(int tt) const { return tt <= lo ? K_SRC : (tt > hi ? K_SNK : K_REAL); }
     __device__ __forceinline__ int knb(int i, int tt) const { return tt <= nlo[i] ? K_SRC : (tt > nhi[i] ? K_SNK : K_REAL); }
     __device__ __forceinline__ int nidx(int i) const { return nc[i] * LPT + t - 1; }
     // segment boundary lanes whose t+1 / t-1 neighbour lives in another segment
-    __device__ __forceinline__ bool top_edge() const { return R > 1 && j == LP - 1 && s + 1 < R && valid; }
-    __device__ __forceinline__ bool bot_edge() const { return R > 1 && j == 0 && s > 0 && valid; }
+    __device__ __forceinline__ bool top_edge() const { return !RW && R > 1 && j == LP - 1 && s + 1 < R && valid; }
+    __device__ __forceinline__ bool bot_edge() const {
+        return RW ? (j == 0 && t > 1 && valid) : (R > 1 && j == 0 && s > 0 && valid);
+    }
+    // bit word / bit of this lane's position in the site's absolute bit words
+    __device__ __forceinline__ int bword(const Prob &p) const { return RW ? ((t - 1) >> 5) * p.P + c : wi; }
+    __device__ __forceinline__ int bbit() const { return RW ? ((t - 1) & 31) : j; }
 };
+
+// a segment ballot (bit j = lane j) as the site's absolute bit words (RW mode:
+// shifted by lo); returns word w of it
+template <int RW>
+__device__ __forceinline__ uint32_t abs_word(uint32_t rel, int lo, int w) {
+    if (!RW) return rel;
+    const unsigned long long a = (unsigned long long)rel << lo;
+    return (uint32_t)(a >> (32 * w));
+}
 
 // global load of solver state; CG = bypass L1 (the asynchronous pulses: other
 // SMs and this warp's own atomics update the state between two reads)
@@ -104,14 +126,14 @@ __device__ __forceinline__ int ldx(const int32_t *p) { return CG ? __ldcg(p) : *
 
 // value at position t+1 / t-1 of the same array: shuffle inside the segment,
 // load across a segment boundary (every lane executes the shuffle)
-template <bool CG = false, int LP, int R, bool WIN>
-__device__ __forceinline__ int up_of(const Lane<LP, R, WIN> &L, int v, const int32_t *arr, int idx, bool ok = true) {
+template <bool CG = false, int LP, int R, bool WIN, int RW>
+__device__ __forceinline__ int up_of(const Lane<LP, R, WIN, RW> &L, int v, const int32_t *arr, int idx, bool ok = true) {
     int r = from_above<LP>(v);
     if (ok && L.top_edge()) r = ldx<CG>(arr + idx + 1);
     return r;
 }
-template <bool CG = false, int LP, int R, bool WIN>
-__device__ __forceinline__ int dn_of(const Lane<LP, R, WIN> &L, int v, const int32_t *arr, int idx) {
+template <bool CG = false, int LP, int R, bool WIN, int RW>
+__device__ __forceinline__ int dn_of(const Lane<LP, R, WIN, RW> &L, int v, const int32_t *arr, int idx) {
     int r = from_below<LP>(v);
     if (L.bot_edge()) r = ldx<CG>(arr + idx - 1);
     return r;
@@ -131,7 +153,7 @@ struct TailQ {
 
 // Residuals of the 14 arcs of a lane's node, target heights and kinds.
 // All shuffles are executed by every lane (uniform control flow).
-template <int LP, int R, bool WIN, bool CG = false>
+template <int LP, int R, bool WIN, bool CG = false, int RW = 0>
 struct Arcs {
     int r[A_COUNT], hv[A_COUNT];
     unsigned snk;   // bit j: arc j leads into the sink (arcs into the source have r = 0)
@@ -141,7 +163,7 @@ struct Arcs {
     int w_dbr_up, w_darL_up, w_dbd_up, w_dadU_up;       // same arrays at position t+1
     int h_u;
 
-    __device__ __forceinline__ void load(const Prob &p, const Arr3 &a, const Lane<LP, R, WIN> &L) {
+    __device__ __forceinline__ void load(const Prob &p, const Arr3 &a, const Lane<LP, R, WIN, RW> &L) {
         const int I = L.I;
         const bool v = L.valid;
         w_cu = v ? ldx<CG>(a.cu + I) : 0;
@@ -223,8 +245,8 @@ struct Arcs {
 };
 
 // site and position of a lateral arc's target
-template <int LP, int R, bool WIN>
-__device__ __forceinline__ void lateral_target(const Lane<LP, R, WIN> &L, int jarc, int &site, int &pos) {
+template <int LP, int R, bool WIN, int RW>
+__device__ __forceinline__ void lateral_target(const Lane<LP, R, WIN, RW> &L, int jarc, int &site, int &pos) {
     const int i = (jarc - A_SR) & 3;
     site = L.nc[i];
     pos = jarc <= A_SU ? L.t : (jarc <= A_UU ? L.t + 1 : L.t - 1);
@@ -255,18 +277,46 @@ __device__ __forceinline__ uint32_t seg_ballot(bool pred) {
 // init of one warp group (LP = 16: two sites; LP = 32: one site, all R
 // segments in order): residuals from the volume, source saturation, greedy
 // upward chain wave (carried across segments), constant offset.
-template <int LP, int R, bool WIN>
+template <int LP, int R, bool WIN, int RW = 0>
 __device__ void w_init(const Prob &p, const Arr3 &a, int c_base, int nsites, long long &flow, long long &offset,
                        long long &presat) {
     int carry = 0;   // wave flow entering the bottom of the next segment
 #pragma unroll 1
     for (int s = 0; s < R; ++s) {
-        Lane<LP, R, WIN> L;
+        Lane<LP, R, WIN, RW> L;
         L.init(p, c_base, nsites, s);
         const int I = L.I;
+        if (RW) {
+            // window-relative lanes cover only the window: initialise the whole row
+            // and fold the terminal arcs of every position into the offset here
+            constexpr int LPT = Lane<LP, R, WIN, RW>::LPT;
+            const int lane = threadIdx.x & 31, cs = c_base + lane / LP;
+            if (lane / LP < nsites && cs < p.P) {
+                for (int k = L.j; k < LPT; k += LP) {
+                    const int idx = cs * LPT + k;
+                    a.cu[idx] = (k + 1 < p.M) ? a.vol[idx + 1] : 0;
+                    a.ph[idx] = p.pen; a.pv[idx] = p.pen;
+                    a.dar[idx] = 0; a.dbr[idx] = 0; a.dad[idx] = 0; a.dbd[idx] = 0;
+                    a.ein0[idx] = 0; a.ein1[idx] = 0;
+                    a.h[idx] = HINF;
+                    a.e[idx] = 0;
+                }
+                const long long icap_off = p.hard ? UNCUTTABLE : (long long)p.inh;
+                if (L.j == 0 && L.lo == L.hi) offset += a.vol[cs * LPT + L.lo];
+                for (int t = L.j + 1; t <= p.L; t += LP)
+                    for (int i = 0; i < 4; i += 2) {   // forward neighbours right (0), down (2)
+                        if (!L.has[i]) continue;
+                        const int ka = L.kown(t), kb = L.knb(i, t);
+                        if ((ka == K_SRC && kb == K_SNK) || (ka == K_SNK && kb == K_SRC)) offset += p.pen;
+                        if (L.kown(t) == K_SRC && L.knb(i, t - 1) == K_SNK) offset += icap_off;
+                        if (L.knb(i, t) == K_SRC && L.kown(t - 1) == K_SNK) offset += icap_off;
+                    }
+            }
+            __syncwarp();
+        }
         const int volj = (L.valid && L.t - 1 < p.M) ? a.vol[I] : 0;
         const int vol_above = up_of(L, volj, a.vol, I);
-        if (L.valid) {
+        if (!RW && L.valid) {
             a.cu[I] = (L.t < p.M) ? vol_above : 0;
             a.ph[I] = p.pen; a.pv[I] = p.pen;
             a.dar[I] = 0; a.dbr[I] = 0; a.dad[I] = 0; a.dbd[I] = 0;
@@ -275,13 +325,13 @@ __device__ void w_init(const Prob &p, const Arr3 &a, int c_base, int nsites, lon
         }
         long long e = 0;
         // chain arc lo: source -> position lo+1 carries vol[lo]
-        const int vol_lo_src = L.valid ? a.vol[L.c * Lane<LP, R, WIN>::LPT + L.lo] : 0;
+        const int vol_lo_src = L.valid ? a.vol[L.c * Lane<LP, R, WIN, RW>::LPT + L.lo] : 0;
         if (L.real && L.t == L.lo + 1) e += vol_lo_src;
         if (WIN && L.valid) {
             const long long icap_off = p.hard ? UNCUTTABLE : (long long)p.inh;
             const int icap = p.hard ? p.hcap : p.inh;
-            if (L.t == 1 && L.lo == L.hi) offset += vol_lo_src;
-            if (L.t <= p.L) {
+            if (!RW && L.t == 1 && L.lo == L.hi) offset += vol_lo_src;
+            if (!RW && L.t <= p.L) {
                 const int t = L.t;
                 for (int i = 0; i < 4; i += 2) {   // forward neighbours right (0), down (2)
                     if (!L.has[i]) continue;
@@ -323,9 +373,9 @@ __device__ void w_init(const Prob &p, const Arr3 &a, int c_base, int nsites, lon
 // ---------------------------------------------------------------------------
 // mask build of one (segment, site) group: pending inbox merge, 13 arc-mask
 // words, excess word, BFS reset words.
-template <int LP, int R, bool WIN>
+template <int LP, int R, bool WIN, int RW = 0>
 __device__ void w_build(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base, int nsites, int seg) {
-    Lane<LP, R, WIN> L;
+    Lane<LP, R, WIN, RW> L;
     L.init(p, c_base, nsites, seg);
     const int I = L.I, P = p.P;
     // every global load of the group is issued before the first store (one
@@ -333,7 +383,7 @@ __device__ void w_build(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
     const uint32_t in0 = L.valid ? a.IN0[L.wi] : 0u, in1 = L.valid ? a.IN1[L.wi] : 0u;
     int e = L.valid ? a.e[I] : 0;
     const int x0 = L.valid ? a.ein0[I] : 0, x1 = L.valid ? a.ein1[I] : 0;
-    Arcs<LP, R, WIN> A;
+    Arcs<LP, R, WIN, false, RW> A;
     A.load(p, a, L);
     // merge both inbox buffers (pushes since the last merge).  Values are merged
     // whether or not their inbox bit is set: an asynchronous pulse can consume a
@@ -347,7 +397,21 @@ __device__ void w_build(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
 #pragma unroll
     for (int q = 0; q < 13; ++q) m[q] = seg_ballot<LP>(L.real && A.r[q] > 0);
     const uint32_t ex = seg_ballot<LP>(L.real && e > 0);
-    if (L.valid && L.j == 0) {
+    if (RW && L.valid && L.j == 0) {
+        // window-relative ballots -> the site's absolute words
+#pragma unroll
+        for (int w = 0; w < RW; ++w) {
+            const int wi = w * P + L.c;
+#pragma unroll
+            for (int q = 0; q < 13; ++q) b.mask[((size_t)q * RW + w) * P + L.c] = abs_word<RW>(m[q], L.lo, w);
+            b.EX[wi] = abs_word<RW>(ex, L.lo, w);
+            b.V[wi] = 0u;
+            b.A[wi] = 0u;
+            a.IN0[wi] = 0u;
+            a.IN1[wi] = 0u;
+            b.F0[wi] = BW<RW ? RW : 1>::range(L.hi, p.M).w[w];
+        }
+    } else if (!RW && L.valid && L.j == 0) {
 #pragma unroll
         for (int q = 0; q < 13; ++q) b.mask[((size_t)q * R + L.s) * P + L.c] = m[q];
         b.EX[L.wi] = ex;
@@ -361,22 +425,23 @@ __device__ void w_build(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
 
 // ---------------------------------------------------------------------------
 // one pulse on a warp group of chains
-template <int LP, int R, bool WIN, bool ASYNC = false, bool DETPUSH = false>
+template <int LP, int R, bool WIN, bool ASYNC = false, bool DETPUSH = false, int RW = 0>
 __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base, int nsites, int seg, int parity,
                         long long &flow, long long &pushes, long long &relabels, uint32_t *dirty,
                         const TailQ *tq = nullptr) {
-    Lane<LP, R, WIN> L;
+    Lane<LP, R, WIN, RW> L;
     L.init(p, c_base, nsites, seg);
     const int I = L.I, P = p.P;
-    constexpr int LPT = Lane<LP, R, WIN>::LPT;
+    constexpr int LPT = Lane<LP, R, WIN, RW>::LPT;
     // synchronous pulses double-buffer the inbox by parity; asynchronous ones use
     // one buffer consumed atomically
     uint32_t *IN_prev = (ASYNC || parity) ? a.IN0 : a.IN1;
     uint32_t *IN_cur = (ASYNC || DETPUSH || !parity) ? a.IN0 : a.IN1;
     int32_t *ein_prev = (ASYNC || parity) ? a.ein0 : a.ein1;
     int32_t *ein_cur = (ASYNC || DETPUSH || !parity) ? a.ein0 : a.ein1;
+    constexpr int NWB = Lane<LP, R, WIN, RW>::NWB;
     int e, xin;
-    Arcs<LP, R, WIN, ASYNC> A;
+    Arcs<LP, R, WIN, ASYNC, RW> A;
     if (DETPUSH) {
         // deterministic push phase: inboxes are merged by the commit phase
         e = L.valid ? a.e[I] : 0;
@@ -384,7 +449,10 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
         A.load(p, a, L);
     } else if (ASYNC) {
         uint32_t inb = 0u;
-        if (L.valid && L.j == 0) inb = atomicExch(&IN_prev[L.wi], 0u);
+        if (L.valid && L.j == 0) {
+            if (RW) for (int w = 0; w < NWB; ++w) inb |= atomicExch(&IN_prev[w * P + L.c], 0u);
+            else inb = atomicExch(&IN_prev[L.wi], 0u);
+        }
         e = L.valid ? __ldcg(a.e + I) : 0;
         xin = L.valid ? atomicExch(&ein_prev[I], 0) : 0;
         A.load(p, a, L);
@@ -393,12 +461,17 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
     } else {
         // all loads before the first store: one round trip per group (ein_prev has
         // no writer during this pulse, so reading it unconditionally is safe)
-        const uint32_t inb = L.valid ? IN_prev[L.wi] : 0u;
+        const uint32_t inw = L.valid ? IN_prev[L.bword(p)] : 0u;
         e = L.valid ? a.e[I] : 0;
         xin = L.valid ? ein_prev[I] : 0;
         A.load(p, a, L);
-        if ((inb >> L.j) & 1u) { e += xin; ein_prev[I] = 0; }
-        if (L.valid && L.j == 0 && inb) IN_prev[L.wi] = 0u;
+        if ((inw >> L.bbit()) & 1u) { e += xin; ein_prev[I] = 0; }
+        if (RW) {
+            if (L.valid && L.j == 0)
+                for (int w = 0; w < NWB; ++w) IN_prev[w * P + L.c] = 0u;
+        } else if (L.valid && L.j == 0 && inw) {
+            IN_prev[L.wi] = 0u;
+        }
     }
     const int hu = A.h_u;
     const bool live = L.real && hu < HINF;
@@ -452,9 +525,9 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
         if (jj == A_DN) continue;
         if ((A.snk >> jj) & 1u) { flow += d; continue; }
         int site, pos;
-        lateral_target<LP, R, WIN>(L, jj, site, pos);
+        lateral_target(L, jj, site, pos);
         atomicAdd(&ein_cur[site * LPT + pos - 1], d);
-        atomicOr(&IN_cur[((pos - 1) / LP) * P + site], 1u << ((pos - 1) % LP));
+        atomicOr(&IN_cur[((pos - 1) >> 5) * P + site], 1u << ((pos - 1) & 31));
         if (tq) tq->push(LP == 16 ? site >> 1 : ((pos - 1) / LP) * P + site);
     }
     // chain-down pushes arrive at lane j-1 (adds to its excess and to its chain-up
@@ -465,7 +538,7 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
         e += dn_in;
         cu_new += dn_in;
     }
-    if (dn > 0 && L.bot_edge()) {
+    if (!RW && dn > 0 && L.bot_edge()) {
         atomicAdd(&a.cu[I - 1], dn);   // (the segment below applies its own cu change atomically too)
         atomicAdd(&ein_cur[I - 1], dn);
         atomicOr(&IN_cur[L.wi - P], 1u << (LP - 1));
@@ -519,10 +592,18 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
         if (dadU_up_d) a.dad[L.nidx(3) + 1] = A.w_dadU_up + dadU_up_d;
     }
     const uint32_t newA = seg_ballot<LP>(L.real && e > 0 && hnew < HINF && (!DETPUSH || pushed));
-    if (L.valid && L.j == 0) b.A[L.wi] = newA;
-    if (DETPUSH) {   // relabel candidates for the relabel phase
-        const uint32_t rl = seg_ballot<LP>(live && !pushed && e > 0);
-        if (L.valid && L.j == 0) b.RL[L.wi] = rl;
+    uint32_t rl = 0u;
+    if (DETPUSH) rl = seg_ballot<LP>(live && !pushed && e > 0);   // relabel candidates for the relabel phase
+    if (L.valid && L.j == 0) {
+        if (RW) {
+            for (int w = 0; w < NWB; ++w) {
+                b.A[w * P + L.c] = abs_word<RW>(newA, L.lo, w);
+                if (DETPUSH) b.RL[w * P + L.c] = abs_word<RW>(rl, L.lo, w);
+            }
+        } else {
+            b.A[L.wi] = newA;
+            if (DETPUSH) b.RL[L.wi] = rl;
+        }
     }
     if (tq && __any_sync(FULL, newA != 0u) && (threadIdx.x & 31) == 0)
         tq->push(LP == 16 ? c_base >> 1 : L.wi);
@@ -531,7 +612,7 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
     const uint32_t pm = seg_ballot<LP>(pushed);
     if (pm && L.valid && L.j == 0) {
 #pragma unroll
-        for (int q = 0; q < R; ++q) {
+        for (int q = 0; q < NWB; ++q) {
             dirty[q * P + L.c] = 1u;
 #pragma unroll
             for (int i = 0; i < 4; ++i)
@@ -543,15 +624,15 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
 // Deterministic relabel phase (capped solves): relabel candidates of the push
 // phase take one above their lowest residual neighbour; the state is settled
 // (no pushes run in this phase) and heights are written to h2 (commit phase).
-template <int LP, int R, bool WIN>
+template <int LP, int R, bool WIN, int RW = 0>
 __device__ void w_relabel(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base, int nsites, int seg,
                           int32_t *h2, long long &relabels) {
-    Lane<LP, R, WIN> L;
+    Lane<LP, R, WIN, RW> L;
     L.init(p, c_base, nsites, seg);
-    const uint32_t rl = L.valid ? b.RL[L.wi] : 0u;
-    Arcs<LP, R, WIN> A;
+    const uint32_t rl = L.valid ? b.RL[L.bword(p)] : 0u;
+    Arcs<LP, R, WIN, false, RW> A;
     A.load(p, a, L);
-    if (L.valid && ((rl >> L.j) & 1u)) {
+    if (L.valid && ((rl >> L.bbit()) & 1u)) {
         int best = HINF;
 #pragma unroll
         for (int jj = 0; jj < A_COUNT; ++jj)
@@ -563,22 +644,31 @@ __device__ void w_relabel(const Prob &p, const Arr3 &a, const Bits2 &b, int c_ba
 
 // Deterministic commit phase: relabeled heights take effect, inboxes merge, and
 // the active bits of the touched nodes are recomputed.
-template <int LP, int R, bool WIN>
+template <int LP, int R, bool WIN, int RW = 0>
 __device__ void w_commit(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base, int nsites, int seg, int32_t *h2) {
-    Lane<LP, R, WIN> L;
+    Lane<LP, R, WIN, RW> L;
     L.init(p, c_base, nsites, seg);
     const int I = L.I;
-    const uint32_t rl = L.valid ? b.RL[L.wi] : 0u, inb = L.valid ? a.IN0[L.wi] : 0u;
-    const bool r_ = (rl >> L.j) & 1u, i_ = (inb >> L.j) & 1u;
+    const uint32_t rl = L.valid ? b.RL[L.bword(p)] : 0u, inb = L.valid ? a.IN0[L.bword(p)] : 0u;
+    const bool r_ = (rl >> L.bbit()) & 1u, i_ = (inb >> L.bbit()) & 1u;
     int h = L.valid ? a.h[I] : HINF, e = L.valid ? a.e[I] : 0;
     if (r_) { h = h2[I]; a.h[I] = h; h2[I] = 0; }
     if (i_) { e += a.ein0[I]; a.ein0[I] = 0; a.e[I] = e; }
     const uint32_t touched = seg_ballot<LP>(r_ || i_);
     const uint32_t act = seg_ballot<LP>((r_ || i_) && L.real && e > 0 && h < HINF);
     if (L.valid && L.j == 0) {
-        b.A[L.wi] = (b.A[L.wi] & ~touched) | act;
-        b.RL[L.wi] = 0u;
-        a.IN0[L.wi] = 0u;
+        if (RW) {
+            for (int w = 0; w < RW; ++w) {
+                const int wi = w * p.P + L.c;
+                b.A[wi] = (b.A[wi] & ~abs_word<RW>(touched, L.lo, w)) | abs_word<RW>(act, L.lo, w);
+                b.RL[wi] = 0u;
+                a.IN0[wi] = 0u;
+            }
+        } else {
+            b.A[L.wi] = (b.A[L.wi] & ~touched) | act;
+            b.RL[L.wi] = 0u;
+            a.IN0[L.wi] = 0u;
+        }
     }
 }
 

@@ -671,6 +671,7 @@ __global__ void k_source_caps(const int32_t *__restrict__ vol, int rows, int col
     }
     warp_add_u64(&out[0], (long long)fin);
     warp_add_u64(&out[1], (long long)inf);
+    if (c < P && lo) atomicMax(&out[2], (unsigned long long)(hi[c] - lo[c]));   // widest window
 }
 
 // (rows, cols, m) -> planar [k][rows*cols]
@@ -874,7 +875,7 @@ struct Pending {
 // h_ctr, labels to labels_out; collect with solve_finish after the stream.
 int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy *en, const gz_sched *sc,
                  const int32_t *lo, const int32_t *hi, int32_t *labels_out, cudaStream_t s, int hcap, int conc,
-                 unsigned long long *h_ctr, Pending *pd) {
+                 unsigned long long *h_ctr, Pending *pd, int max_width = -1) {
     Prob p;
     memset(&p, 0, sizeof(p));
     p.Y = rows; p.G = cols; p.M = m; p.L = m - 1; p.P = rows * cols;
@@ -951,6 +952,7 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
 #define GZ_PICK(W_, NW_, D_) if (win == W_ && NW == NW_ && det == D_) kern = (const void *)gz2::gz_bitsolve_kernel<W_, NW_, D_>;
 #define GZ_PICK_NW(NW_) GZ_PICK(false, NW_, false) GZ_PICK(false, NW_, true) GZ_PICK(true, NW_, false) GZ_PICK(true, NW_, true)
     const int LPn = lanes_for(m);
+    bool rel = false;   // window-relative instance (set below)
     // two CTAs per SM (64 registers, smaller BFS regions) for the m <= 16 instance
     // (spills cost ~12% on a lone solve; with concurrent pair solves the doubled
     // warp count wins ~12%: bench A/B, round 1)
@@ -964,6 +966,14 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
         GZ_PICK4(16, 1, 1) GZ_PICK4(16, 1, 2) GZ_PICK4(32, 1, 1) GZ_PICK4(32, 2, 1) GZ_PICK4(32, 4, 1)
         GZ_PICK4(32, 8, 1)
 #undef GZ_PICK4
+        // windowed solves whose windows are at most 15 positions wide (the level-1/2
+        // fine solves): window-relative 16-lane groups over the absolute rows
+        if (win && max_width >= 0 && max_width <= 15 && (LPn == 32 || LPn == 64) && !getenv("GZ_NO_REL")) {
+            kern = LPn == 32 ? (const void *)gz4::gz_tilesolve_kernel<16, 1, true, 1, 1>
+                             : (const void *)gz4::gz_tilesolve_kernel<16, 1, true, 1, 2>;
+            rel = true;
+            (void)rel;
+        }
     } else if (which == 2) {
         GZ_PICK_NW(1) GZ_PICK_NW(2) GZ_PICK_NW(4) GZ_PICK_NW(8)
     } else {
@@ -1058,10 +1068,10 @@ int solve_finish(Pending &pd, gz_stats *st) {
 // Synchronous solve (one problem, all SMs).
 int solve_planar(const Workspace &w, int rows, int cols, int m, const gz_energy *en, const gz_sched *sc,
                  const int32_t *lo, const int32_t *hi, int32_t *labels_out, gz_stats *st, cudaStream_t s,
-                 int hcap = HARD_CAP_DEFAULT) {
+                 int hcap = HARD_CAP_DEFAULT, int max_width = -1) {
     unsigned long long h_ctr[gz::CTR_COUNT];
     Pending pd;
-    int rc = solve_launch(w, rows, cols, m, en, sc, lo, hi, labels_out, s, hcap, 1, h_ctr, &pd);
+    int rc = solve_launch(w, rows, cols, m, en, sc, lo, hi, labels_out, s, hcap, 1, h_ctr, &pd, max_width);
     if (rc) return rc;
     if (pd.progress) {   // debug: poll instead of blocking, report where blocks stall
         const double limit = atof(getenv("GZ_DEBUG_PROGRESS"));
@@ -1147,11 +1157,11 @@ int gz_solve_volume(const int32_t *vol, int32_t rows, int32_t cols, int32_t m, c
     }
     // int32 device state: the total source capacity bounds every excess,
     // residual and flow value, so it must fit (and picks the hard stand-in)
-    CK(cudaMemsetAsync(w.ctr, 0, 16, s));
+    CK(cudaMemsetAsync(w.ctr, 0, 24, s));
     k_source_caps<<<(P + 255) / 256, 256, 0, s>>>(vol, rows, cols, m, lo, hi, *energy, w.ctr);
     CK(cudaGetLastError());
-    unsigned long long census[2];
-    CK(cudaMemcpyAsync(census, w.ctr, 16, cudaMemcpyDeviceToHost, s));
+    unsigned long long census[3];
+    CK(cudaMemcpyAsync(census, w.ctr, 24, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     const unsigned long long lim = 0x7fffffffull;
     int hcap = HARD_CAP_DEFAULT;
@@ -1163,7 +1173,8 @@ int gz_solve_volume(const int32_t *vol, int32_t rows, int32_t cols, int32_t m, c
     } else if (census[0] >= lim) {
         return GZ_ERR_OVERFLOW;
     }
-    return solve_planar(w, rows, cols, m, energy, sched, lo, hi, labels_out, stats_out, s, hcap);
+    return solve_planar(w, rows, cols, m, energy, sched, lo, hi, labels_out, stats_out, s, hcap,
+                        lo ? (int)census[2] : -1);
 }
 
 int gz_solve_pairs(const uint8_t *left, const uint8_t *right, int32_t batch, int32_t img_h, int32_t img_w,

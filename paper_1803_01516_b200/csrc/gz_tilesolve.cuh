@@ -246,9 +246,10 @@ __device__ unsigned bfs_round(const Prob &p, const Arr3 &a, const Bits2 &b, cons
 // ---------------------------------------------------------------------------
 // The solver.  LP = 16: two sites per warp group (m <= 16); LP = 32: one
 // (segment, site) per warp group, R segments per chain (m <= 32 R).
-template <int LP, int R, bool WIN, int OCC>
+template <int LP, int R, bool WIN, int OCC, int RW = 0>
 __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 b, Arr3 a, Geo g, unsigned long long *bar) {
-    constexpr int NW = R, LPT = LP * R;
+    // RW > 0: window-relative 16-lane groups over rows of 32 RW positions (gz_chain.cuh)
+    constexpr int NW = RW ? RW : R, LPT = RW ? 32 * RW : LP * R;
     __shared__ unsigned s_f3[3], s_r3[3], s_qn[2];
     __shared__ int s_q[BLOCK];   // per-round pool of active groups (<= 32 per warp)
     __shared__ unsigned s_tn[2];  // tail-mode worklist lengths
@@ -298,9 +299,15 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
         const int grp_ = gwid + it_ * gnw;                                                       \
         uint32_t wk_ = 0u;                                                                       \
         if (it_ < giter && grp_ < ngroups) {                                                     \
-            const int w0_ = LP == 16 ? 2 * grp_ : grp_;                                          \
-            wk_ = __ldcg((W1) + w0_) | __ldcg((W2) + w0_);                                       \
-            if (LP == 16 && w0_ + 1 < p.P) wk_ |= __ldcg((W1) + w0_ + 1) | __ldcg((W2) + w0_ + 1); \
+            if (LP == 16) {                                                                      \
+                for (int w_ = 0; w_ < NW; ++w_) {                                                \
+                    const int q_ = w_ * p.P + 2 * grp_;                                          \
+                    wk_ |= __ldcg((W1) + q_) | __ldcg((W2) + q_);                                \
+                    if (2 * grp_ + 1 < p.P) wk_ |= __ldcg((W1) + q_ + 1) | __ldcg((W2) + q_ + 1); \
+                }                                                                                \
+            } else {                                                                             \
+                wk_ = __ldcg((W1) + grp_) | __ldcg((W2) + grp_);                                 \
+            }                                                                                    \
         }                                                                                        \
         const uint32_t msk_ = __ballot_sync(FULL, wk_ != 0u);                                    \
         CNT += __popc(msk_);                                                                     \
@@ -323,7 +330,7 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
 
     FOR_TILES {
         const TileBox tb(p, g, tile);
-        for_tile_groups<LP>(p, tb, [&](int cb, int ns) { gz3::w_init<LP, R, WIN>(p, a, cb, ns, flow, offset, presat); });
+        for_tile_groups<LP>(p, tb, [&](int cb, int ns) { gz3::w_init<LP, R, WIN, RW>(p, a, cb, ns, flow, offset, presat); });
     }
     for (int w = ttid; w < nwords; w += tstride) b.IN[w] = 1u;   // every site starts dirty
     TEAM_SYNC();
@@ -353,9 +360,14 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
             long long dummy = 0;
             int dummy2 = 0;
             auto build = [&](int cb, int sg) {
-                gz3::w_build<LP, R, WIN>(p, a, b, cb, CPW, sg);
-                const int w0 = sg * p.P + cb;
-                if (lane < CPW && cb + lane < p.P) b.IN[w0 + lane] = 0u;
+                gz3::w_build<LP, R, WIN, RW>(p, a, b, cb, CPW, sg);
+                if (RW) {   // dirty marks: every bit word of both sites
+                    if (lane < CPW && cb + lane < p.P)
+                        for (int w = 0; w < NW; ++w) b.IN[w * p.P + cb + lane] = 0u;
+                } else {
+                    const int w0 = sg * p.P + cb;
+                    if (lane < CPW && cb + lane < p.P) b.IN[w0 + lane] = 0u;
+                }
             };
             FOR_ACTIVE_GROUPS(b.IN, b.IN, dummy, dummy2, build)
         }
@@ -432,7 +444,7 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
             // active or inbox bits run a pulse.
             const uint32_t *IN_prev = parity ? a.IN0 : a.IN1;
             auto pulse_fn = [&](int cb, int sg) {
-                gz3::w_pulse<LP, R, WIN>(p, a, b, cb, CPW, sg, parity, flow, pushes, relabels, b.IN);
+                gz3::w_pulse<LP, R, WIN, false, false, RW>(p, a, b, cb, CPW, sg, parity, flow, pushes, relabels, b.IN);
             };
             long long upd0 = updates;
             int cta_groups = 0;
@@ -441,22 +453,22 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
                 // each phase reading state no concurrent phase writes
                 int32_t *h2 = a.ein1;   // the second inbox plane is idle in this mode
                 auto push_fn = [&](int cb, int sg) {
-                    gz3::w_pulse<LP, R, WIN, false, true>(p, a, b, cb, CPW, sg, 0, flow, pushes, relabels, b.IN);
+                    gz3::w_pulse<LP, R, WIN, false, true, RW>(p, a, b, cb, CPW, sg, 0, flow, pushes, relabels, b.IN);
                 };
                 FOR_ACTIVE_GROUPS(b.A, b.A, updates, cta_groups, push_fn)
                 TEAM_SYNC();
                 long long dmy = 0;
                 int dmy2 = 0;
-                auto relabel_fn = [&](int cb, int sg) { gz3::w_relabel<LP, R, WIN>(p, a, b, cb, CPW, sg, h2, relabels); };
+                auto relabel_fn = [&](int cb, int sg) { gz3::w_relabel<LP, R, WIN, RW>(p, a, b, cb, CPW, sg, h2, relabels); };
                 FOR_ACTIVE_GROUPS(b.RL, b.RL, dmy, dmy2, relabel_fn)
                 TEAM_SYNC();
-                auto commit_fn = [&](int cb, int sg) { gz3::w_commit<LP, R, WIN>(p, a, b, cb, CPW, sg, h2); };
+                auto commit_fn = [&](int cb, int sg) { gz3::w_commit<LP, R, WIN, RW>(p, a, b, cb, CPW, sg, h2); };
                 FOR_ACTIVE_GROUPS(b.RL, a.IN0, dmy, dmy2, commit_fn)
             } else if (p.async_l > 0) {
                 // asynchronous pulse: async_l scan-and-process iterations per team
                 // barrier; pushes between warps are picked up within the pulse
                 auto pulse_async = [&](int cb, int sg) {
-                    gz3::w_pulse<LP, R, WIN, true>(p, a, b, cb, CPW, sg, 0, flow, pushes, relabels, b.IN);
+                    gz3::w_pulse<LP, R, WIN, true, false, RW>(p, a, b, cb, CPW, sg, 0, flow, pushes, relabels, b.IN);
                 };
                 for (int ai = 0; ai < p.async_l; ++ai) {
                     FOR_ACTIVE_GROUPS(b.A, a.IN0, updates, cta_groups, pulse_async)
@@ -491,9 +503,15 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
                     const int it_ = it0 + lane, grp_ = gwid + it_ * gnw;
                     uint32_t wk_ = 0u;
                     if (it_ < giter && grp_ < ngroups) {
-                        const int w0_ = LP == 16 ? 2 * grp_ : grp_;
-                        wk_ = b.A[w0_] | INn[w0_];
-                        if (LP == 16 && w0_ + 1 < p.P) wk_ |= b.A[w0_ + 1] | INn[w0_ + 1];
+                        if (LP == 16) {
+                            for (int w_ = 0; w_ < NW; ++w_) {
+                                const int q_ = w_ * p.P + 2 * grp_;
+                                wk_ |= b.A[q_] | INn[q_];
+                                if (2 * grp_ + 1 < p.P) wk_ |= b.A[q_ + 1] | INn[q_ + 1];
+                            }
+                        } else {
+                            wk_ = b.A[grp_] | INn[grp_];
+                        }
                     }
                     const uint32_t msk_ = __ballot_sync(FULL, wk_ != 0u);
                     int base_ = 0;
@@ -524,7 +542,7 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
                                 old = __shfl_sync(FULL, old, 0);
                                 if ((old >> (gg & 31)) & 1u) continue;   // already processed this pulse
                                 const int cb = LP == 16 ? 2 * gg : gg % p.P, sg = LP == 16 ? 0 : gg / p.P;
-                                gz3::w_pulse<LP, R, WIN>(p, a, b, cb, CPW, sg, parity, flow, pushes, relabels, b.IN, &tq);
+                                gz3::w_pulse<LP, R, WIN, false, false, RW>(p, a, b, cb, CPW, sg, parity, flow, pushes, relabels, b.IN, &tq);
                                 ++updates;
                             }
                             __syncthreads();
@@ -565,7 +583,7 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
     FOR_TILES                                                                       \
     for (int r = TileBox(p, g, tile).y0 + warp, y1_ = TileBox(p, g, tile).y1; r < y1_; r += nwarps) \
         for (int x = TileBox(p, g, tile).x0 + lane, x1_ = TileBox(p, g, tile).x1; x < x1_; x += 32)
-    FOR_TILE_SITES gz3::w_reach_init<R, WIN>(p, b, r * p.G + x);
+    FOR_TILE_SITES gz3::w_reach_init<NW, WIN>(p, b, r * p.G + x);
     TEAM_SYNC();
     int reach_passes = 0;
     int32_t *Rin = b.R0, *Rout = b.R1;

@@ -95,6 +95,9 @@ def graph_size(volume: torch.Tensor, params: EnergyParams, lo: Optional[torch.Te
         emit, s_off, d_off = _pair_counts(lo2[a_sl], hi2[a_sl], lo2[b_sl], hi2[b_sl], m)
         arcs += int(emit.sum())
         offset += params.penalty * int(s_off.sum()) + icap * int(d_off.sum())
+    # the reference accumulates the offset in numba int64 (flownet.py:115, 124-125,
+    # 153-154, 172-173), which wraps once many uncuttable (2^56) arcs fold
+    offset = (offset + (1 << 63)) % (1 << 64) - (1 << 63)
     return n_nodes, 2 * arcs, offset
 
 

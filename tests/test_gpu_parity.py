@@ -134,3 +134,24 @@ def test_capped_solves_are_deterministic(gz, m):
                 runs.append((r.flow, r.labeling.copy(), r.stats["sweeps"], r.stats["pulses"]))
             assert runs[0][0] == runs[1][0] and np.array_equal(runs[0][1], runs[1][1]), (m, cap)
             assert runs[0][2:] == runs[1][2:]
+
+
+@pytest.mark.parametrize("m", [20, 30, 45, 60])
+def test_narrow_windows_match_oracle(gz, oracle, m):
+    """Windows at most 15 positions wide on 17 <= m <= 64 run the window-relative
+    16-lane instance (the level-1/2 fine solves); bit-exact vs the oracle."""
+    rng = np.random.default_rng(500 + m)
+    for k in range(4):
+        rows, cols = int(rng.integers(3, 12)), int(rng.integers(3, 12))
+        vol = rng.integers(0, 150, (rows, cols, m)).astype(np.int64)
+        pen, inh, hard = int(rng.integers(1, 9)), int(rng.integers(0, 60)), k == 3
+        p = gz.EnergyParams(pen, inh, hard)
+        lo = rng.integers(0, m, rows * cols).astype(np.int32)
+        hi = np.minimum(lo + rng.integers(0, 16, rows * cols), m - 1).astype(np.int32)
+        net = gz.build_network(vol, p, lo, hi)
+        got = gz.maxflow_push_relabel(net)
+        onet = oracle.build_network(vol, pen, p.inhibit_capacity, lo, hi)
+        flow, energy, lab, side, _ = oracle.maxflow_push_relabel(onet)
+        assert net.const_offset == onet.const_offset
+        assert got.flow == flow and got.energy == energy, (m, k)
+        assert np.array_equal(got.labeling, lab) and np.array_equal(got.source_side, side)
