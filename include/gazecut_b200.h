@@ -37,7 +37,8 @@ enum gz_status {
     GZ_ERR_CONSISTENCY = -4,  /* InternalConsistencyError (maxflow.py:51-52): cut cost != labeling energy */
     GZ_ERR_OVERFLOW = -5,     /* capacities too large for the int32 device state */
     GZ_ERR_NOCONVERGE = -6,   /* internal iteration guard tripped (never expected) */
-    GZ_ERR_NOGPU = -7         /* no sm_100 device */
+    GZ_ERR_NOGPU = -7,        /* no sm_100 device */
+    GZ_ERR_BANDS = -8         /* row-band launches were not co-resident (team barrier timed out) */
 };
 
 /* geometry.py:61-138 CuboidSpec (the fields the data term needs) */
@@ -118,6 +119,25 @@ int gz_solve_pairs_host(const uint8_t *left_host, const uint8_t *right_host, int
                         int32_t img_w, int32_t channels, const gz_cuboid *cuboid, const gz_energy *energy,
                         const gz_sched *sched, int32_t *labels_host, gz_stats *stats_host, void *workspace,
                         size_t workspace_bytes, void *stream);
+
+/* Row-band solve of ONE volume too large for one GPU (SURVEY.md §8(e),
+ * BASELINE config 5).  Same semantics as gz_solve_volume (replaces
+ * maxflow.py:481-510 solve_exact / maxflow.py:403-478 for exact solves; the
+ * cut is canonical, so the result is bit-identical to the one-launch solve),
+ * but the site rows are split into nbands bands: band k's rows of every state
+ * plane live in the HBM of devices[k] (one virtual range, CUDA VMM) and band k
+ * runs as a cooperative launch on devices[k].  All launches form one team;
+ * arcs across a band edge are read and written in place over NVLink (peer
+ * loads, stores, atomics).  devices may repeat: bands on one GPU split its SMs.
+ * HOST buffers: vol_host (rows, cols, m) int32, lo_host/hi_host (rows, cols)
+ * int32 or both NULL, labels_host (rows, cols) int32 out, stats_out host.
+ * Exact solves only (GZ_SCHED_CAPPED is rejected); m <= 256.
+ * Env GZ_BAND_SPIN_MS: a band that waits this long at a team barrier aborts
+ * the solve with GZ_ERR_BANDS instead of hanging (30000). */
+int gz_solve_volume_banded(const int32_t *vol_host, int32_t rows, int32_t cols, int32_t m,
+                           const gz_energy *energy, const gz_sched *sched, const int32_t *lo_host,
+                           const int32_t *hi_host, int32_t nbands, const int32_t *devices,
+                           int32_t *labels_host, gz_stats *stats_out);
 
 /* energy.py:129-155 total_energy on device.  Writes one int64 to energy_out (device). */
 int gz_total_energy(const int32_t *labels, const int32_t *vol, int32_t rows, int32_t cols, int32_t m,

@@ -39,6 +39,7 @@ from .maxflow import (
     maxflow_push_relabel,
     maxflow_reference,
     solve_exact,
+    solve_exact_bands,
     source_side,
 )
 from .pairs import PairSolver, solve_pairs
@@ -53,6 +54,6 @@ __all__ = [
     "expected_arc_count", "expected_node_count", "extract_labeling", "full_windows", "make_scene",
     "maxflow_push_relabel", "maxflow_reference", "network_from_arcs", "pairwise_term",
     "pixels_from_gaze_depth", "sad_volume", "sad_volume_device", "solve_exact", "solve_level1",
-    "solve_level2", "solve_pairs", "source_side", "thin_skin", "total_energy", "whs_from_disparity",
+    "solve_level2", "solve_exact_bands", "solve_pairs", "source_side", "thin_skin", "total_energy", "whs_from_disparity",
     "__version__",
 ]

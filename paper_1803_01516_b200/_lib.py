@@ -21,6 +21,7 @@ GZ_ERR_CONSISTENCY = -4
 GZ_ERR_OVERFLOW = -5
 GZ_ERR_NOCONVERGE = -6
 GZ_ERR_NOGPU = -7
+GZ_ERR_BANDS = -8
 GZ_SCHED_NO_WAVE = 1
 GZ_SCHED_CAPPED = 2
 GZ_SCHED_V1 = 4
@@ -87,6 +88,9 @@ def lib():
                                      _vp, C.c_size_t, _vp]
         L.gz_solve_pairs_host.restype = C.c_int
         L.gz_solve_pairs_host.argtypes = L.gz_solve_pairs.argtypes
+        L.gz_solve_volume_banded.restype = C.c_int
+        L.gz_solve_volume_banded.argtypes = [_vp, _i32, _i32, _i32, C.POINTER(Energy), C.POINTER(Sched),
+                                             _vp, _vp, _i32, _vp, _vp, C.POINTER(Stats)]
         L.gz_total_energy.restype = C.c_int
         L.gz_total_energy.argtypes = [_vp, _vp, _i32, _i32, _i32, C.POINTER(Energy), _vp, _vp]
         L.gz_coarsen.restype = C.c_int
@@ -115,6 +119,6 @@ def check(status: int, where: str) -> None:
 # Every symbol include/gazecut_b200.h declares (checked by tests/test_abi.py).
 EXPORTED = (
     "gz_workspace_bytes", "gz_sad_volume", "gz_solve_volume", "gz_solve_pairs",
-    "gz_solve_pairs_host", "gz_total_energy", "gz_coarsen", "gz_thin_skin",
+    "gz_solve_pairs_host", "gz_solve_volume_banded", "gz_total_energy", "gz_coarsen", "gz_thin_skin",
     "gz_status_string", "gz_build_info",
 )

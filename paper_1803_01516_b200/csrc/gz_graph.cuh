@@ -84,6 +84,7 @@ enum Ctr : int {
     CTR_T0 = 24,        // 6 phase timers (ns): init, mask build, bfs, pulses, reach, tail
     CTR_TRACE = 35,     // debug trace accumulator (GZ_TRACE=2)
     CTR_TQN = 36,       // tail-mode global worklist length
+    CTR_ABORT = 37,     // multi-launch (row-band) team gave up waiting at a barrier
     CTR_UPDATES = 30,   // node updates performed by pulses (v4)
     CTR_BAR0 = 32,      // 3 rotating team-barrier words (v4)
     CTR_COUNT = 40

@@ -856,7 +856,43 @@ gz4::Geo tile_geo(int rows, int cols, int nb, int nw, int occ) {
     while (g.TY > 1 && (rows < g.TY + 2 * g.H ? rows : g.TY + 2 * g.H) * rw > regmax) --g.TY;
     g.ny = (rows + g.TY - 1) / g.TY;
     g.ntiles = g.nx * g.ny;
+    // one band: the whole grid (row bands override these, solve_launch)
+    g.nb = nb; g.rank0 = 0;
+    g.t0 = 0; g.t1 = g.ntiles;
+    g.c0 = 0; g.c1 = rows * cols;
+    g.gg0 = 0; g.gg1 = (rows * cols + 1) / 2;
+    g.sys = 0; g.spin_ms = 0;
     return g;
+}
+
+// Row-band plan of one problem: band k is a cooperative launch
+// of grid[k] CTAs on dev[k] / stream[k]; all launches form one team.  Band k owns
+// tile rows [ny k / n, ny (k+1) / n) of the team's tile geometry.
+constexpr int MAX_BANDS = 64;
+struct BandPlan {
+    int n = 0;
+    int dev[MAX_BANDS], grid[MAX_BANDS];
+    cudaStream_t stream[MAX_BANDS];
+    int home = 0;       // device of the caller's stream
+    int multi_dev = 0;  // bands on more than one device: system-scope fences
+    int spin_ms = 30000;
+    gz4::Geo geo;       // team geometry (nb = sum of grid)
+};
+
+// Band k's share of the team geometry.
+gz4::Geo band_geo(const gz4::Geo &g, int rows, int cols, int n, int k, int rank0, int multi_dev, int spin_ms) {
+    gz4::Geo b = g;
+    const int ty0 = (int)((long long)g.ny * k / n), ty1 = (int)((long long)g.ny * (k + 1) / n);
+    const int P = rows * cols;
+    b.t0 = ty0 * g.nx; b.t1 = ty1 * g.nx;
+    b.c0 = (ty0 * g.TY < rows ? ty0 * g.TY : rows) * cols;
+    b.c1 = (ty1 * g.TY < rows ? ty1 * g.TY : rows) * cols;
+    b.gg0 = b.c0 / 2;                                   // a pair straddling a band edge goes to the lower band
+    b.gg1 = k + 1 == n ? (P + 1) / 2 : b.c1 / 2;
+    b.rank0 = rank0;
+    b.sys = multi_dev;
+    b.spin_ms = n > 1 ? spin_ms : 0;
+    return b;
 }
 
 // Solve one problem whose volume is already in w.vol (layout of the chosen solver).
@@ -875,7 +911,7 @@ struct Pending {
 // h_ctr, labels to labels_out; collect with solve_finish after the stream.
 int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy *en, const gz_sched *sc,
                  const int32_t *lo, const int32_t *hi, int32_t *labels_out, cudaStream_t s, int hcap, int conc,
-                 unsigned long long *h_ctr, Pending *pd, int max_width = -1) {
+                 unsigned long long *h_ctr, Pending *pd, int max_width = -1, const BandPlan *bp = nullptr) {
     Prob p;
     memset(&p, 0, sizeof(p));
     p.Y = rows; p.G = cols; p.M = m; p.L = m - 1; p.P = rows * cols;
@@ -1007,7 +1043,31 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
     void *args1[] = {&p};
     void *args2[] = {&p, &bb};
     void *args4[] = {&p, &bb, &a3, &geo, &bar};
-    if (which == 4) {
+    if (which == 4 && bp) {
+        // row bands: one cooperative launch per band, forked from and joined to s
+        if (occ4 != 1 || bp->geo.ny < bp->n) return GZ_ERR_ARG;
+        cudaEvent_t fork;
+        CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+        CK(cudaEventRecord(fork, s));
+        cudaEvent_t joins[MAX_BANDS];
+        int rank0 = 0;
+        for (int k = 0; k < bp->n; ++k) {
+            CK(cudaSetDevice(bp->dev[k]));
+            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem));
+            CK(cudaStreamWaitEvent(bp->stream[k], fork, 0));
+            gz4::Geo gk = band_geo(bp->geo, rows, cols, bp->n, k, rank0, bp->multi_dev, bp->spin_ms);
+            void *argsk[] = {&p, &bb, &a3, &gk, &bar};
+            CK(cudaLaunchCooperativeKernel(kern, dim3(bp->grid[k]), dim3(threads), argsk, dyn_smem, bp->stream[k]));
+            CK(cudaEventCreateWithFlags(&joins[k], cudaEventDisableTiming));
+            CK(cudaEventRecord(joins[k], bp->stream[k]));
+            rank0 += bp->grid[k];
+        }
+        CK(cudaSetDevice(bp->home));
+        for (int k = 0; k < bp->n; ++k) CK(cudaStreamWaitEvent(s, joins[k], 0));
+        for (int k = 0; k < bp->n; ++k) cudaEventDestroy(joins[k]);
+        cudaEventDestroy(fork);
+        grid = rank0;
+    } else if (which == 4) {
         if (geo.ntiles < grid) grid = geo.ntiles;   // every CTA owns at least one tile
         geo = tile_geo(rows, cols, grid, words_for(m), occ4);
         CK(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(threads), args4, dyn_smem, s));
@@ -1038,6 +1098,7 @@ int solve_finish(Pending &pd, gz_stats *st) {
     cudaEventDestroy(pd.e0);
     cudaEventDestroy(pd.e1);
     const unsigned long long *h_ctr = pd.h_ctr;
+    if (h_ctr[CTR_ABORT]) return GZ_ERR_BANDS;
     if (h_ctr[CTR_STATUS]) return -(int)h_ctr[CTR_STATUS];
     if (st) {
         memset(st, 0, sizeof(*st));
@@ -1333,6 +1394,7 @@ const char *gz_status_string(int status) {
     case GZ_ERR_OVERFLOW: return "capacities exceed the int32 device state";
     case GZ_ERR_NOCONVERGE: return "iteration guard tripped";
     case GZ_ERR_NOGPU: return "no sm_100 GPU";
+    case GZ_ERR_BANDS: return "row-band launches were not co-resident (team barrier timed out)";
     }
     return "unknown status";
 }
@@ -1340,3 +1402,5 @@ const char *gz_status_string(int status) {
 const char *gz_build_info(void) { return "gazecut_b200 v4 sm_100a tile-owned persistent push-relabel (temporally blocked BFS)"; }
 
 }  // extern "C"
+
+#include "gz_bands.cuh"

@@ -48,8 +48,19 @@ __host__ __device__ constexpr int region_sites(int nw, int occ) {
                           : BLOCK;
 }
 
+// Tile geometry plus the row band this launch owns.  One problem may be solved
+// by several co-resident cooperative launches (row bands): the
+// team is all CTAs of all launches (nb, global rank = rank0 + blockIdx.x), and
+// each launch works its own tile rows [t0, t1), sites [c0, c1) and pair groups
+// [gg0, gg1) (LP = 16).  A single launch is the one-band case (rank0 = 0,
+// nb = gridDim.x, the whole grid).
 struct Geo {
     int TY, TX, ny, nx, ntiles, H;
+    int nb, rank0;         // team size (all bands), first global rank of this launch
+    int t0, t1, c0, c1;    // this band's tiles and sites
+    int gg0, gg1;          // this band's site-pair groups (LP = 16)
+    int sys;               // bands on several GPUs: system-scope fences in the team barrier
+    int spin_ms;           // multi-launch team: abort a barrier wait after this long (0: never)
 };
 
 // Team barrier with a fused 2-bit OR reduction.  Barrier k uses word k % 3 of
@@ -61,7 +72,10 @@ struct Geo {
 // clears it for barrier k+2 (nobody reaches k+2 before rank 0 reaches k+1).
 struct Team {
     unsigned long long *bar;   // 3 rotating words of this team
+    unsigned long long *abort_flag;   // set when a multi-launch team gives up (spin_ns)
     int nb, rank;
+    int sys;                   // system-scope fences (team spans GPUs)
+    unsigned long long spin_ns;   // > 0: give up a barrier after this long (multi-launch teams)
     // returns the number of CTAs that raised flag 0 (bits 0-15) and flag 1 (16-31)
     __device__ __forceinline__ unsigned sync_count(unsigned flags, int &phase, unsigned *s_f3, unsigned *s_r3) const {
         const int k3 = phase % 3;
@@ -74,14 +88,34 @@ struct Team {
             const unsigned long long inc = (rank == 0 ? 0x80000000ull - (unsigned long long)(nb - 1) : 1ull) |
                                            ((f & 1u) ? 1ull << 32 : 0ull) | ((f & 2u) ? 1ull << 48 : 0ull);
             unsigned long long *word = bar + k3;
-            __threadfence();
-            const unsigned long long old = atomicAdd(word, inc);
-            unsigned long long cur;
-            do {
-                cur = *(volatile unsigned long long *)word;
-            } while (((old ^ cur) & 0x80000000ull) == 0ull);
-            if (rank == 0) bar[(k3 + 2) % 3] = 0ull;
-            __threadfence();
+            if (sys) __threadfence_system(); else __threadfence();
+            unsigned long long cur = 0ull;
+            bool aborted = spin_ns && *(volatile unsigned long long *)abort_flag;
+            if (!aborted) {
+                // (an aborted team's barriers all return "nothing happened", so every
+                // loop of the solve ends and the launch exits)
+                const unsigned long long old = atomicAdd(word, inc);
+                unsigned long long t0 = 0ull;
+                unsigned spins = 0;
+                do {
+                    cur = *(volatile unsigned long long *)word;
+                    if (spin_ns && ((++spins & 4095u) == 0u)) {
+                        // a multi-launch team whose other launches never arrived (not
+                        // co-resident): abort instead of hanging the GPU
+                        unsigned long long t;
+                        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                        if (t0 == 0ull) t0 = t;
+                        if (t - t0 > spin_ns || *(volatile unsigned long long *)abort_flag) {
+                            atomicExch(abort_flag, 1ull);
+                            aborted = true;
+                            break;
+                        }
+                    }
+                } while (((old ^ cur) & 0x80000000ull) == 0ull);
+                if (aborted) cur = 0ull;
+                else if (rank == 0) bar[(k3 + 2) % 3] = 0ull;
+            }
+            if (sys) __threadfence_system(); else __threadfence();
             s_r3[k3] = (unsigned)(cur >> 32);   // CTAs with flag 0 (low 16) / flag 1 (high 16)
         }
         __syncthreads();
@@ -261,17 +295,18 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
     int phase = 0;
     constexpr int RS = region_sites(NW, OCC);
     uint32_t *sF0 = s_dyn, *sF1 = s_dyn + NW * RS, *sM = s_dyn + 2 * NW * RS;
-    const bool resident = g.ntiles <= (int)gridDim.x;   // one tile per CTA: masks stay in smem for the sweep
-    const Team tm{bar, (int)gridDim.x, (int)blockIdx.x};
+    const bool resident = g.t1 - g.t0 <= (int)gridDim.x;   // one tile per CTA: masks stay in smem for the sweep
+    const Team tm{bar, p.ctr + CTR_ABORT, g.nb, g.rank0 + (int)blockIdx.x, g.sys,
+                  (unsigned long long)g.spin_ms * 1000000ull};
 #define TEAM_SYNC() (void)tm.sync_or(0u, phase, s_f3, s_r3)
 #define TEAM_OR(f) tm.sync_or((f), phase, s_f3, s_r3)
 #define TEAM_COUNT(f) tm.sync_count((f), phase, s_f3, s_r3)
     unsigned long long t_prev = 0, t_acc[6] = {0, 0, 0, 0, 0, 0};
-    const bool timer = blockIdx.x == 0 && threadIdx.x == 0;
+    const bool timer = tm.rank == 0 && threadIdx.x == 0;
     if (timer) t_prev = gz2::gtimer();
     if (timer) p.t_start_ns = t_prev;
 #define TICK(slot) do { if (timer) { unsigned long long t_ = gz2::gtimer(); t_acc[slot] += t_ - t_prev; t_prev = t_; } } while (0)
-#define FOR_TILES for (int tile = tm.rank; tile < g.ntiles; tile += tm.nb)
+#define FOR_TILES for (int tile = g.t0 + (int)blockIdx.x; tile < g.t1; tile += (int)gridDim.x)
     long long flow = 0, offset = 0, presat = 0, pushes = 0, relabels = 0;
     volatile unsigned long long *vctr = p.ctr;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -279,9 +314,15 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
     const int nwords = NW * p.P;   // one bit word per (segment, site)
     // warp groups: LP = 16 -> pairs of sites; LP = 32 -> (segment, site) words
     const int ngroups = LP == 16 ? (p.P + 1) / 2 : nwords;
-    const int gnw = tm.nb * nwarps, gwid = tm.rank * nwarps + warp;
-    const int giter = (ngroups + gnw - 1) / gnw;
-    const int ttid = tm.rank * blockDim.x + threadIdx.x, tstride = tm.nb * blockDim.x;
+    // this band's groups, interleaved over the warps of this launch: local index li
+    // -> site pair gg0 + li (LP = 16), or (segment, site) word of the band's sites
+    const int bsites = g.c1 - g.c0, bwords = NW * bsites;
+    const int nloc = LP == 16 ? g.gg1 - g.gg0 : bwords;
+    const int gnw = (int)gridDim.x * nwarps, gwid = (int)blockIdx.x * nwarps + warp;
+    const int giter = (nloc + gnw - 1) / gnw;
+    auto band_word = [&](int i) { const int s_ = i / bsites; return s_ * p.P + g.c0 + (i - s_ * bsites); };
+    auto grp_of = [&](int li) { return LP == 16 ? g.gg0 + li : band_word(li); };
+    const int ttid = (int)blockIdx.x * blockDim.x + threadIdx.x, tstride = (int)gridDim.x * blockDim.x;
     // tail mode: claim bitmap + two worklists in the (then idle) BFS shared memory
     const int tail_bw = (ngroups + 31) / 32;
     const int tail_cap = min(4096, ((int)(smem_bytes(OCC) / 4) - tail_bw) / 2);
@@ -296,9 +337,10 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
 #define FOR_ACTIVE_GROUPS(W1, W2, CNT, CTAN, FN)                                                         \
     for (int it0 = 0; it0 < giter; it0 += 32, ++qround) {                                        \
         const int it_ = it0 + lane;                                                              \
-        const int grp_ = gwid + it_ * gnw;                                                       \
+        const int li_ = gwid + it_ * gnw;                                                        \
+        const int grp_ = li_ < nloc ? grp_of(li_) : 0;                                           \
         uint32_t wk_ = 0u;                                                                       \
-        if (it_ < giter && grp_ < ngroups) {                                                     \
+        if (it_ < giter && li_ < nloc) {                                                         \
             if (LP == 16) {                                                                      \
                 for (int w_ = 0; w_ < NW; ++w_) {                                                \
                     const int q_ = w_ * p.P + 2 * grp_;                                          \
@@ -332,7 +374,7 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
         const TileBox tb(p, g, tile);
         for_tile_groups<LP>(p, tb, [&](int cb, int ns) { gz3::w_init<LP, R, WIN, RW>(p, a, cb, ns, flow, offset, presat); });
     }
-    for (int w = ttid; w < nwords; w += tstride) b.IN[w] = 1u;   // every site starts dirty
+    for (int i = ttid; i < bwords; i += tstride) b.IN[band_word(i)] = 1u;   // every site starts dirty
     TEAM_SYNC();
     TICK(0);
     int sweeps = 0, levels_total = 0, pulses = 0, parity = 0;
@@ -344,8 +386,8 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
         // (every inbox is merged by the builds below, so the inbox parity restarts)
         parity = 0;
         if (threadIdx.x == 0 && tm.rank == 0) p.ctr[CTR_TQN] = 0ull;
-        for (int w = ttid; w < nwords; w += tstride) {
-            const int c = w % p.P, s = w / p.P;
+        for (int i = ttid; i < bwords; i += tstride) {
+            const int s = i / bsites, c = g.c0 + (i - s * bsites), w = s * p.P + c;
             const int hi = WIN ? p.hi[c] : p.L;
             b.F0[w] = BW<NW>::range(hi, p.M).w[s];
             b.V[w] = 0u;
@@ -353,8 +395,8 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
         {
             const int4 hinf4 = make_int4(HINF, HINF, HINF, HINF);
             int4 *h4 = reinterpret_cast<int4 *>(a.h);
-            const int n4 = p.P * (LPT / 4);
-            for (int q = ttid; q < n4; q += tstride) h4[q] = hinf4;
+            const int n4 = g.c1 * (LPT / 4);
+            for (int q = g.c0 * (LPT / 4) + ttid; q < n4; q += tstride) h4[q] = hinf4;
         }
         {
             long long dummy = 0;
@@ -429,7 +471,8 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
         if (err) break;
         if (!found && exhausted) break;
         if (p.capped && sweeps >= p.max_sweeps) { converged = 0; break; }
-        for (int w = ttid; w < nwords; w += tstride) {
+        for (int i = ttid; i < bwords; i += tstride) {
+            const int w = band_word(i);
             b.A[w] = Vin[w] & b.EX[w];
             if (p.capped) b.RL[w] = 0u;   // (the BFS used RL as a visited buffer)
         }
@@ -500,9 +543,10 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
                 unsigned *gq_n = (unsigned *)&p.ctr[CTR_TQN];
                 int *gq = (int *)b.F1;   // BFS frontier buffer, idle during pulses
                 for (int it0 = 0; it0 < giter; it0 += 32) {
-                    const int it_ = it0 + lane, grp_ = gwid + it_ * gnw;
+                    const int it_ = it0 + lane, li_ = gwid + it_ * gnw;
+                    const int grp_ = li_ < nloc ? grp_of(li_) : 0;
                     uint32_t wk_ = 0u;
-                    if (it_ < giter && grp_ < ngroups) {
+                    if (it_ < giter && li_ < nloc) {
                         if (LP == 16) {
                             for (int w_ = 0; w_ < NW; ++w_) {
                                 const int q_ = w_ * p.P + 2 * grp_;

@@ -183,3 +183,62 @@ def solve_exact(volume, params: EnergyParams, solver: str = "push-relabel", roun
         raise InternalConsistencyError(f"cut cost {result.energy} != labeling energy {check}")
     result.stats.update(build_s=build_s, nodes=net.n_nodes, arcs=net.num_arcs, const_offset=net.const_offset)
     return result
+
+
+def solve_exact_bands(volume, params: EnergyParams, devices=(0, 1), lo=None, hi=None) -> CutResult:
+    """``solve_exact`` (maxflow.py:481-510) for one volume split into row bands,
+    band k on GPU ``devices[k]`` (BASELINE config 5).
+
+    One cooperative launch per band over that band's tile rows; the launches
+    form one team, and arcs across a band edge are read and written in place
+    over NVLink (gz_solve_volume_banded, include/gazecut_b200.h).  The minimum
+    cut is canonical, so flow, energy and labeling are bit-identical to the
+    one-GPU ``solve_exact``.  ``devices`` may repeat a GPU (its SMs are split
+    between the bands it hosts).  Host arrays in, host arrays out."""
+    t0 = time.perf_counter()
+    vol = np.ascontiguousarray(np.asarray(volume))
+    if vol.ndim != 3:
+        raise ValueError("volume must be (rows, cols, num_labels)")
+    if vol.size and (int(vol.min()) < 0 or int(vol.max()) > np.iinfo(np.int32).max):
+        raise ValueError("data costs must be non-negative and fit the int32 device state")
+    rows, cols, m = (int(s) for s in vol.shape)
+    vol32 = np.ascontiguousarray(vol, dtype=np.int32)
+    lo32 = hi32 = None
+    if lo is not None and hi is not None:
+        lo32 = np.ascontiguousarray(np.asarray(lo).reshape(rows, cols), dtype=np.int32)
+        hi32 = np.ascontiguousarray(np.asarray(hi).reshape(rows, cols), dtype=np.int32)
+        if (lo32 < 0).any() or (hi32 >= m).any() or (lo32 > hi32).any():
+            raise ValueError("label windows must satisfy 0 <= lo <= hi < num_labels")
+        if (lo32 == 0).all() and (hi32 == m - 1).all():
+            lo32 = hi32 = None
+    devs = np.ascontiguousarray(np.asarray(list(devices), dtype=np.int32))
+    if devs.size < 1:
+        raise ValueError("at least one band")
+    _dev.require_gpu()
+    labels = np.empty((rows, cols), dtype=np.int32)
+    st = _lib.Stats()
+    en = params._c()
+    sc = _sched(12, None, True, 0)
+    vp = lambda a: None if a is None else a.ctypes.data  # noqa: E731
+    rc = _lib.lib().gz_solve_volume_banded(vp(vol32), rows, cols, m, C.byref(en), C.byref(sc), vp(lo32), vp(hi32),
+                                          int(devs.size), vp(devs), vp(labels), C.byref(st))
+    if rc == _lib.GZ_ERR_ARG:
+        raise ValueError("gz_solve_volume_banded: invalid argument (m in 2..256, one tile row per band, "
+                         "valid device ids)")
+    _lib.check(rc, "gz_solve_volume_banded")
+    flow = int(st.flow)
+    offset = int(st.const_offset)
+    energy = flow + offset
+    if int(st.labeling_energy) != energy:
+        raise InternalConsistencyError(f"cut cost {energy} != labeling energy {int(st.labeling_energy)}")
+    stats = {
+        "solver": "push-relabel", "bands": int(devs.size), "devices": [int(d) for d in devs],
+        "converged": bool(st.converged), "sweeps": int(st.sweeps), "pushes": int(st.pushes),
+        "relabels": int(st.relabels), "presaturated": int(st.presaturated), "device": "sm_100a",
+        "device_ms": float(st.ms_total), "pulses": int(st.pulses), "bfs_passes": int(st.bfs_passes),
+        "reach_passes": int(st.reach_passes), "labeling_energy": int(st.labeling_energy),
+        "node_updates": int(st.node_updates), "const_offset": offset, "wall_s": time.perf_counter() - t0,
+        "phase_ms": {k: round(float(v), 4) for k, v in
+                     zip(("init", "mask_build", "global_relabel", "pulses", "extract", "tail"), st.ms_phase)},
+    }
+    return CutResult(flow=flow, energy=energy, labeling=labels, stats=stats)
