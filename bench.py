@@ -335,7 +335,7 @@ def main():
                      "traffic": traffic, "kernel": "gz4::gz_tilesolve_kernel", "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": statistics.mean(alg), "state_bytes_S": S,
                      "mean_launch_ms": statistics.mean(kern_ms), "per_launch_achieved": per_launch,
-                     "concurrent_launches": min(8, int(os.environ.get("GZ_PAIR_CONC", "8"))),
+                     "concurrent_launches": min(16, int(os.environ.get("GZ_PAIR_CONC", "8"))),
                      "note": "state (S = 38 MB) is L2-resident; the kernel is barrier/latency bound (DESIGN.md)"},
         "gnups": gnups,
         "clocks": clocks.summary(),

@@ -1259,16 +1259,16 @@ int gz_solve_pairs(const uint8_t *left, const uint8_t *right, int32_t batch, int
     // over 1/conc of the SMs on its own stream with its own workspace slice.
     int conc = 8;   // measured: 1 -> 250, 4 -> 366, 8 -> ~400 pairs/s (C1, 64 pairs per call)
     if (const char *cs = getenv("GZ_PAIR_CONC")) conc = atoi(cs);
-    if (conc > 8) conc = 8;
+    if (conc > 16) conc = 16;
     if ((size_t)conc * one > workspace_bytes) conc = (int)(workspace_bytes / one);
     if (conc > batch) conc = batch;
     if (which != 4 || conc < 1) conc = 1;
-    static cudaStream_t streams[8];
+    static cudaStream_t streams[16];
     static bool have_streams = false;
     static unsigned long long *pinned = nullptr;
     static size_t pinned_n = 0;
     if (conc > 1 && !have_streams) {
-        for (int k = 0; k < 8; ++k) CK(cudaStreamCreateWithFlags(&streams[k], cudaStreamNonBlocking));
+        for (int k = 0; k < 16; ++k) CK(cudaStreamCreateWithFlags(&streams[k], cudaStreamNonBlocking));
         have_streams = true;
     }
     if (pinned_n < (size_t)batch * gz::CTR_COUNT) {

@@ -8,6 +8,8 @@ reference-facing end-to-end call (host buffers in, host labels out).
 
 from __future__ import annotations
 
+import os
+
 import ctypes as C
 from typing import Optional
 
@@ -52,7 +54,7 @@ class PairSolver:
         self.sites = cuboid.y_extent * cuboid.g_extent
         self.ws_one = _lib.lib().gz_workspace_bytes(cuboid.y_extent, cuboid.g_extent, cuboid.num_labels)
         self._ws: Optional[torch.Tensor] = None
-        self.concurrency = 8
+        self.concurrency = int(os.environ.get("GZ_PAIR_CONC", "8"))
 
     def _workspace(self, extra: int = 0, batch: int = 1) -> torch.Tensor:
         # room for up to `concurrency` pair solves in flight (gz_solve_pairs runs

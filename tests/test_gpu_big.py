@@ -78,3 +78,16 @@ def test_c5_data_term_matches_reference(gz):
     for r0 in range(0, vol.shape[0], 64):
         hs.update(np.ascontiguousarray(vol[r0:r0 + 64].cpu().numpy().astype(np.int64)).tobytes())
     assert hs.hexdigest() == g["volume"]
+
+
+def test_c3_two_bands_reproduce_one_gpu_flow(gz):
+    """BASELINE config 3 split into two row bands: the same
+    canonical cut as the one-launch solve (flow 27,476,775, certified above)."""
+    g = BIG["c3_volume"]
+    seed, w, h, dmin, dmax, m = g["args"]
+    sc = gz.make_scene(seed, w, h, dmin, dmax)
+    cub = gz.cuboid_from_disparity_range(w, h, dmin, dmax, num_labels=m)
+    vol = gz.sad_volume_device(sc.left, sc.right, cub).cpu().numpy()
+    r = gz.solve_exact_bands(vol, gz.EnergyParams(14, 1023), devices=(0, 0))
+    assert r.flow == r.energy == r.stats["labeling_energy"] == 27476775
+    print("C3 two bands device_ms", r.stats["device_ms"], "sweeps", r.stats["sweeps"])
