@@ -49,6 +49,13 @@ typedef struct {
     int32_t d_min, m;          /* first depth number, number of labels */
 } gz_cuboid;
 
+/* geometry.py:61-138 CuboidSpec offsets for the ground-truth transform
+ * (imaging.py:155-201); rows/cols = y_extent/g_extent, m = d_extent. */
+typedef struct {
+    int32_t g_min, y_min, d_min, rows, cols, m;
+    int32_t offset1, offset2, offset3, lw_offset, rw_offset, h_offset;
+} gz_gaze;
+
 /* energy.py:37-50 EnergyParams */
 typedef struct {
     int32_t penalty, inhibit, hard_inhibit;
@@ -138,6 +145,30 @@ int gz_solve_volume_banded(const int32_t *vol_host, int32_t rows, int32_t cols, 
                            const gz_energy *energy, const gz_sched *sched, const int32_t *lo_host,
                            const int32_t *hi_host, int32_t nbands, const int32_t *devices,
                            int32_t *labels_host, gz_stats *stats_out);
+
+/* imaging.py:155-201 ground_truth_to_depth on device.  gt: (img_h, img_w)
+ * uint8 disparity * scale, 0 = none.  depth_out (rows, cols) int32 cuboid-local
+ * depth numbers (nearest surface wins), valid_out uint8, counts_out 4 int64:
+ * out_of_range, off_grid, kept pixels, valid sites (collisions = kept - valid).
+ * Device pointers, stream-ordered. */
+int gz_ground_truth_to_depth(const uint8_t *gt, int32_t img_h, int32_t img_w, int32_t scale, const gz_gaze *gaze,
+                             int32_t *depth_out, uint8_t *valid_out, int64_t *counts_out, void *stream);
+
+/* evalreport.py:47-61 error_count for `batch` labelings (batch x rows x cols
+ * int32) against one ground truth.  out: batch x (tail + 3) int64 = total
+ * error, evaluated sites, histogram[0..tail] (|diff| >= tail pooled).
+ * Device pointers, stream-ordered. */
+int gz_error_count(const int32_t *labels, int32_t batch, const int32_t *depth, const uint8_t *valid, int32_t rows,
+                   int32_t cols, int32_t tail, int64_t *out, void *stream);
+
+/* The solves of evalreport.py:88-126 sweep_penalty: one volume (rows, cols, m)
+ * int32 on the device, n energy parameter sets, exact solves (up to 8 in
+ * flight, each on 1/8 of the SMs).  labels_out: n x rows x cols int32 (device),
+ * stats_out: n entries (host).  workspace: k x gz_workspace_bytes(rows, cols, m)
+ * runs k solves at once. */
+int gz_solve_volume_batch(const int32_t *vol, int32_t rows, int32_t cols, int32_t m, const gz_energy *energies,
+                          int32_t n, const gz_sched *sched, int32_t *labels_out, gz_stats *stats_out,
+                          void *workspace, size_t workspace_bytes, void *stream);
 
 /* energy.py:129-155 total_energy on device.  Writes one int64 to energy_out (device). */
 int gz_total_energy(const int32_t *labels, const int32_t *vol, int32_t rows, int32_t cols, int32_t m,

@@ -346,3 +346,39 @@ def solve_level2(volume, penalty, inhibit, block, skin_radius=1, hard=False, rou
 
 if os.environ.get("GZ_ORACLE_BUILD_ON_IMPORT"):
     build_lib()
+
+
+# ---------------------------------------------------------------------------
+# accuracy accounting (numpy restatements; test infrastructure only)
+
+def _round_away_half(a):
+    """geometry.py:37-47: halve, .5 away from zero."""
+    return np.sign(a) * ((np.abs(a) + 1) // 2)
+
+
+def ground_truth_to_depth(gt_image, scale, g_min, y_min, d_min, rows, cols, m, offset1, offset2, offset3,
+                          lw_offset, rw_offset, h_offset):
+    """imaging.py:155-201 -> (depth int32, valid bool, out_of_range, off_grid, collisions)."""
+    gt = np.asarray(gt_image)
+    ys, xs = np.nonzero(gt)
+    dis = (gt[ys, xs].astype(np.int64) * 2 + scale) // (2 * scale)
+    W = xs - _round_away_half(lw_offset + rw_offset) + _round_away_half(dis)
+    S = _round_away_half(lw_offset - rw_offset) - _round_away_half(dis)
+    gi = (W - offset1) - g_min
+    yi = (ys - h_offset + offset2) - y_min
+    k = (S - offset3) - d_min
+    on_grid = (gi >= 0) & (gi < cols) & (yi >= 0) & (yi < rows)
+    in_range = (k >= 0) & (k < m)
+    keep = on_grid & in_range
+    best = np.full((rows, cols), m, dtype=np.int64)
+    np.minimum.at(best, (yi[keep], gi[keep]), k[keep])
+    valid = best < m
+    depth = np.where(valid, best, 0).astype(np.int32)
+    return depth, valid, int((on_grid & ~in_range).sum()), int((~on_grid).sum()), int(keep.sum() - valid.sum())
+
+
+def error_count(labeling, depth, valid, tail=9):
+    """evalreport.py:47-61 -> (total_error, evaluated, histogram[0..tail])."""
+    diff = np.abs(np.asarray(labeling, np.int64) - np.asarray(depth, np.int64))[np.asarray(valid, bool)]
+    hist = np.bincount(np.minimum(diff, tail), minlength=tail + 1)
+    return int(diff.sum()), int(diff.size), hist.astype(np.int64)

@@ -7,8 +7,9 @@ max-flow, min-cut read-out, energy check and hierarchy helpers run as
 hand-written sm_100a CUDA kernels in ``libgazecut_b200.so`` behind a C ABI
 (include/gazecut_b200.h).  There is no CPU fallback.
 
-Out of scope: image I/O (imaging.py), accuracy accounting
-(evalreport.py), the CLI and generic CSR networks.
+Accuracy accounting (ground truth -> depth numbers, error counts, penalty
+sweeps) also runs on the device.  Out of scope: image file I/O,
+CSV reports, the CLI and generic CSR networks.
 """
 
 from .energy import UNCUTTABLE, EnergyParams, pairwise_term, sad_volume, sad_volume_device, total_energy
@@ -31,6 +32,16 @@ from .geometry import (
     pixels_from_gaze_depth,
     whs_from_disparity,
 )
+from .evalreport import (
+    HISTOGRAM_TAIL,
+    ErrorReport,
+    SweepRecord,
+    best_penalty,
+    error_count,
+    error_count_device,
+    error_from_histogram,
+    sweep_penalty,
+)
 from .hierarchy import coarsen, solve_level1, solve_level2, thin_skin
 from .maxflow import (
     CutResult,
@@ -42,12 +53,15 @@ from .maxflow import (
     solve_exact_bands,
     source_side,
 )
+from .imaging import GroundTruthDepth, ground_truth_to_depth
 from .pairs import PairSolver, solve_pairs
 from .synthetic import SyntheticScene, make_scene
 
 __version__ = "0.1.0"
 
 __all__ = [
+    "HISTOGRAM_TAIL", "ErrorReport", "SweepRecord", "GroundTruthDepth", "best_penalty", "error_count",
+    "error_count_device", "error_from_histogram", "ground_truth_to_depth", "sweep_penalty",
     "CuboidSpec", "CutResult", "EnergyParams", "FlowNetwork", "GazeDepthCoord", "InternalConsistencyError",
     "PairSolver", "SyntheticScene", "UNCUTTABLE", "WhsCoord", "build_network", "coarsen",
     "cross_from_pixels", "cuboid_from_disparity_range", "cuboid_with_offsets", "disparity_from_whs",

@@ -34,6 +34,12 @@ class Cuboid(C.Structure):
                 ("width", "height", "g_min", "g_extent", "y_min", "y_extent", "d_min", "m")]
 
 
+class Gaze(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in
+                ("g_min", "y_min", "d_min", "rows", "cols", "m", "offset1", "offset2", "offset3",
+                 "lw_offset", "rw_offset", "h_offset")]
+
+
 class Energy(C.Structure):
     _fields_ = [("penalty", C.c_int32), ("inhibit", C.c_int32), ("hard_inhibit", C.c_int32)]
 
@@ -91,6 +97,13 @@ def lib():
         L.gz_solve_volume_banded.restype = C.c_int
         L.gz_solve_volume_banded.argtypes = [_vp, _i32, _i32, _i32, C.POINTER(Energy), C.POINTER(Sched),
                                              _vp, _vp, _i32, _vp, _vp, C.POINTER(Stats)]
+        L.gz_ground_truth_to_depth.restype = C.c_int
+        L.gz_ground_truth_to_depth.argtypes = [_vp, _i32, _i32, _i32, C.POINTER(Gaze), _vp, _vp, _vp, _vp]
+        L.gz_error_count.restype = C.c_int
+        L.gz_error_count.argtypes = [_vp, _i32, _vp, _vp, _i32, _i32, _i32, _vp, _vp]
+        L.gz_solve_volume_batch.restype = C.c_int
+        L.gz_solve_volume_batch.argtypes = [_vp, _i32, _i32, _i32, _vp, _i32, C.POINTER(Sched), _vp, _vp,
+                                            _vp, C.c_size_t, _vp]
         L.gz_total_energy.restype = C.c_int
         L.gz_total_energy.argtypes = [_vp, _vp, _i32, _i32, _i32, C.POINTER(Energy), _vp, _vp]
         L.gz_coarsen.restype = C.c_int
@@ -119,6 +132,7 @@ def check(status: int, where: str) -> None:
 # Every symbol include/gazecut_b200.h declares (checked by tests/test_abi.py).
 EXPORTED = (
     "gz_workspace_bytes", "gz_sad_volume", "gz_solve_volume", "gz_solve_pairs",
-    "gz_solve_pairs_host", "gz_solve_volume_banded", "gz_total_energy", "gz_coarsen", "gz_thin_skin",
+    "gz_solve_pairs_host", "gz_solve_volume_banded", "gz_ground_truth_to_depth",
+    "gz_error_count", "gz_solve_volume_batch", "gz_total_energy", "gz_coarsen", "gz_thin_skin",
     "gz_status_string", "gz_build_info",
 )

@@ -5,6 +5,7 @@
 
 from __future__ import annotations
 
+import hashlib
 import os
 import shutil
 import subprocess
@@ -27,14 +28,18 @@ def nvcc() -> str:
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
-    newest = max(p.stat().st_mtime for p in SOURCES + HEADERS)
-    if not force and OUT.exists() and OUT.stat().st_mtime >= newest:
+    # rebuild when the sources' content differs from what the library was built
+    # from (a content digest, not mtimes: an edit during a running build counts)
+    digest = hashlib.sha256(b"".join(p.read_bytes() for p in SOURCES + HEADERS)).hexdigest()
+    stamp = OUT.with_suffix(".so.src")
+    if not force and OUT.exists() and stamp.exists() and stamp.read_text() == digest:
         return OUT
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
            f"-I{ROOT / 'include'}", "-o", str(OUT), *map(str, SOURCES)]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.run(cmd, check=True)
+    stamp.write_text(digest)
     return OUT
 
 

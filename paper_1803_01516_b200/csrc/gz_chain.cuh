@@ -491,8 +491,8 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
             if ((A.snk >> A_UP) & 1u) {
                 flow += x_out;
             } else if (L.top_edge()) {   // into the next segment's first node
-                atomicAdd(&ein_cur[I + 1], x_out);
-                atomicOr(&IN_cur[L.wi + P], 1u);
+                gz_atomic_add(p, &ein_cur[I + 1], x_out);
+                gz_atomic_or(p, &IN_cur[L.wi + P], 1u);
                 if (tq) tq->push(L.wi + P);
             }
         }
@@ -526,8 +526,8 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
         if ((A.snk >> jj) & 1u) { flow += d; continue; }
         int site, pos;
         lateral_target(L, jj, site, pos);
-        atomicAdd(&ein_cur[site * LPT + pos - 1], d);
-        atomicOr(&IN_cur[((pos - 1) >> 5) * P + site], 1u << ((pos - 1) & 31));
+        gz_atomic_add(p, &ein_cur[site * LPT + pos - 1], d);
+        gz_atomic_or(p, &IN_cur[((pos - 1) >> 5) * P + site], 1u << ((pos - 1) & 31));
         if (tq) tq->push(LP == 16 ? site >> 1 : ((pos - 1) / LP) * P + site);
     }
     // chain-down pushes arrive at lane j-1 (adds to its excess and to its chain-up
@@ -539,9 +539,9 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
         cu_new += dn_in;
     }
     if (!RW && dn > 0 && L.bot_edge()) {
-        atomicAdd(&a.cu[I - 1], dn);   // (the segment below applies its own cu change atomically too)
-        atomicAdd(&ein_cur[I - 1], dn);
-        atomicOr(&IN_cur[L.wi - P], 1u << (LP - 1));
+        gz_atomic_add(p, &a.cu[I - 1], dn);   // (the segment below applies its own cu change atomically too)
+        gz_atomic_add(p, &ein_cur[I - 1], dn);
+        gz_atomic_or(p, &IN_cur[L.wi - P], 1u << (LP - 1));
         if (tq) tq->push(L.wi - P);
     }
     // relabel a live node that could not push (deterministic mode: a later phase)

@@ -74,7 +74,21 @@ struct Prob {
     int32_t *e, *ein, *h, *h2;
     int32_t *reach, *reach2, *labels;
     unsigned long long *ctr;  // counters, see CTR_*
+    int sys;                  // row bands spanning GPUs: system-scope global atomics (gz_atomic_*)
 };
+
+// Global-memory atomics of the v4 solver that can land in another GPU's band
+// (inboxes, chain residuals, counters): system scope when the team spans GPUs,
+// so peer-memory atomics are formally atomic against the owner GPU's own.
+// One uniform branch otherwise.
+template <typename T>
+__device__ __forceinline__ T gz_atomic_add(const Prob &p, T *a, T v) {
+    return p.sys ? atomicAdd_system(a, v) : atomicAdd(a, v);
+}
+template <typename T>
+__device__ __forceinline__ T gz_atomic_or(const Prob &p, T *a, T v) {
+    return p.sys ? atomicOr_system(a, v) : atomicOr(a, v);
+}
 
 enum Ctr : int {
     CTR_FLOW = 0, CTR_OFFSET, CTR_PRESAT, CTR_PUSHES, CTR_RELABELS, CTR_ENERGY, CTR_HARDVIOL,

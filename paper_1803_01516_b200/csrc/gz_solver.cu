@@ -457,11 +457,14 @@ __device__ void phase_energy_col(const Prob &p, int c, long long &energy, int &v
     }
 }
 
-__device__ __forceinline__ void warp_add_u64(unsigned long long *dst, long long v) {
+__device__ __forceinline__ void warp_add_u64(unsigned long long *dst, long long v, int sys = 0) {
     unsigned long long x = (unsigned long long)v;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
-    if ((threadIdx.x & 31) == 0 && x) atomicAdd(dst, x);
+    if ((threadIdx.x & 31) == 0 && x) {
+        if (sys) atomicAdd_system(dst, x);
+        else atomicAdd(dst, x);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -674,6 +677,11 @@ __global__ void k_source_caps(const int32_t *__restrict__ vol, int rows, int col
     if (c < P && lo) atomicMax(&out[2], (unsigned long long)(hi[c] - lo[c]));   // widest window
 }
 
+__global__ void k_fill_i32(int32_t *dst, int n, int32_t v) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = v;
+}
+
 // (rows, cols, m) -> planar [k][rows*cols]
 __global__ void k_to_planar(const int32_t *__restrict__ src, int P, int M, int32_t *__restrict__ dst) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -838,12 +846,11 @@ int choose_solver(int m, const gz_sched *sc) {
     return 4;
 }
 
-// Tile geometry of the v4 solver for a team of nb CTAs.
-gz4::Geo tile_geo(int rows, int cols, int nb, int nw, int occ) {
+// Tile geometry of the v4 solver for a team of nb CTAs, BFS blocking depth H.
+gz4::Geo tile_geo_h(int rows, int cols, int nb, int nw, int occ, int H) {
     const int regmax = gz4::region_sites(nw, occ);
     gz4::Geo g;
-    const char *hs = getenv("GZ_BFS_H");
-    g.H = hs ? atoi(hs) : 8;
+    g.H = H;
     g.TX = 32;
     // the smallest region (one tile row plus halo) must fit the BFS register tiles
     while (g.H > 1 && (1 + 2 * g.H) * (g.TX + 2 * g.H) > regmax) --g.H;
@@ -856,6 +863,19 @@ gz4::Geo tile_geo(int rows, int cols, int nb, int nw, int occ) {
     while (g.TY > 1 && (rows < g.TY + 2 * g.H ? rows : g.TY + 2 * g.H) * rw > regmax) --g.TY;
     g.ny = (rows + g.TY - 1) / g.TY;
     g.ntiles = g.nx * g.ny;
+    return g;
+}
+
+// H = 8 when every CTA owns one tile (its arc masks stay in shared memory for
+// the whole sweep, so deep blocking saves team barriers).  When CTAs cycle
+// through several tiles the masks are reloaded every round and the halo of a
+// deep round dwarfs its tile: H = 3 (NW >= 2) / 4 (NW = 1) measured best
+// (C3 21.4 -> 10.4 s, C3q 2.41 -> 1.73 s, C2 68 -> 57 ms, bench C1 472 -> 486
+// pairs/s; tools/sweep_cfg.py, round 1).  GZ_BFS_H overrides.
+gz4::Geo tile_geo(int rows, int cols, int nb, int nw, int occ) {
+    const char *hs = getenv("GZ_BFS_H");
+    gz4::Geo g = tile_geo_h(rows, cols, nb, nw, occ, hs ? atoi(hs) : 8);
+    if (!hs && g.ntiles > nb) g = tile_geo_h(rows, cols, nb, nw, occ, nw >= 2 ? 3 : 4);
     // one band: the whole grid (row bands override these, solve_launch)
     g.nb = nb; g.rank0 = 0;
     g.t0 = 0; g.t1 = g.ntiles;
@@ -1045,6 +1065,7 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
     void *args4[] = {&p, &bb, &a3, &geo, &bar};
     if (which == 4 && bp) {
         // row bands: one cooperative launch per band, forked from and joined to s
+        p.sys = bp->multi_dev;
         if (occ4 != 1 || bp->geo.ny < bp->n) return GZ_ERR_ARG;
         cudaEvent_t fork;
         CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
@@ -1404,3 +1425,4 @@ const char *gz_build_info(void) { return "gazecut_b200 v4 sm_100a tile-owned per
 }  // extern "C"
 
 #include "gz_bands.cuh"
+#include "gz_eval.cuh"

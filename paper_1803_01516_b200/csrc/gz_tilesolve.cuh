@@ -94,7 +94,7 @@ struct Team {
             if (!aborted) {
                 // (an aborted team's barriers all return "nothing happened", so every
                 // loop of the solve ends and the launch exits)
-                const unsigned long long old = atomicAdd(word, inc);
+                const unsigned long long old = sys ? atomicAdd_system(word, inc) : atomicAdd(word, inc);
                 unsigned long long t0 = 0ull;
                 unsigned spins = 0;
                 do {
@@ -106,7 +106,7 @@ struct Team {
                         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
                         if (t0 == 0ull) t0 = t;
                         if (t - t0 > spin_ns || *(volatile unsigned long long *)abort_flag) {
-                            atomicExch(abort_flag, 1ull);
+                            atomicExch_system(abort_flag, 1ull);
                             aborted = true;
                             break;
                         }
@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
                     }
                     const uint32_t msk_ = __ballot_sync(FULL, wk_ != 0u);
                     int base_ = 0;
-                    if (lane == 0 && msk_) base_ = (int)atomicAdd(gq_n, (unsigned)__popc(msk_));
+                    if (lane == 0 && msk_) base_ = (int)gz_atomic_add(p, gq_n, (unsigned)__popc(msk_));
                     base_ = __shfl_sync(FULL, base_, 0);
                     if ((msk_ >> lane) & 1u) gq[base_ + __popc(msk_ & ((1u << lane) - 1u))] = grp_;
                 }
@@ -661,14 +661,14 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
 #undef TICK
     if (timer)
         for (int q = 0; q < 6; ++q) p.ctr[CTR_T0 + q] = t_acc[q];
-    warp_add_u64(&p.ctr[CTR_FLOW], flow);
-    warp_add_u64(&p.ctr[CTR_OFFSET], offset);
-    warp_add_u64(&p.ctr[CTR_PRESAT], presat);
-    warp_add_u64(&p.ctr[CTR_PUSHES], pushes);
-    warp_add_u64(&p.ctr[CTR_RELABELS], relabels);
-    warp_add_u64(&p.ctr[CTR_ENERGY], energy);
-    warp_add_u64(&p.ctr[CTR_STRANDED], stranded);
-    if (lane == 0 && updates) atomicAdd(&p.ctr[CTR_UPDATES], (unsigned long long)updates * CPW * (LP < p.L ? LP : p.L));
+    warp_add_u64(&p.ctr[CTR_FLOW], flow, p.sys);
+    warp_add_u64(&p.ctr[CTR_OFFSET], offset, p.sys);
+    warp_add_u64(&p.ctr[CTR_PRESAT], presat, p.sys);
+    warp_add_u64(&p.ctr[CTR_PUSHES], pushes, p.sys);
+    warp_add_u64(&p.ctr[CTR_RELABELS], relabels, p.sys);
+    warp_add_u64(&p.ctr[CTR_ENERGY], energy, p.sys);
+    warp_add_u64(&p.ctr[CTR_STRANDED], stranded, p.sys);
+    if (lane == 0 && updates) gz_atomic_add(p, &p.ctr[CTR_UPDATES], (unsigned long long)updates * CPW * (LP < p.L ? LP : p.L));
     if (viol) p.ctr[CTR_HARDVIOL] = 1;
     if (threadIdx.x == 0 && tm.rank == 0) {
         p.ctr[CTR_SWEEPS] = sweeps;

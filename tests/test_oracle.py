@@ -85,3 +85,31 @@ def test_ladder24_recorded_energies(oracle):
     l2 = oracle.solve_level2(vol, 14, 1023, 3)
     assert l2["energy"] == lad["l2b3"]["energy"] == 790883
     assert sha(l2["labeling"].astype(np.int32)) == lad["l2b3"]["labeling"]
+
+
+def test_oracle_accuracy_matches_reference_fixtures():
+    """oracle.ground_truth_to_depth / error_count against tests/golden/eval.json
+    (produced by the reference itself, oracle/make_golden_eval.py)."""
+    import hashlib
+    import json
+    from pathlib import Path
+
+    from oracle import oracle as o
+    from paper_1803_01516_b200.geometry import cuboid_from_disparity_range
+    from paper_1803_01516_b200.synthetic import make_scene
+
+    E = json.loads((Path(__file__).resolve().parent / "golden" / "eval.json").read_text())
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()  # noqa: E731
+    for g in E["ground_truth"]:
+        seed, w, h, dmin, dmax, m = g["args"]
+        sc = make_scene(seed, width=w, height=h, dis_min=dmin, dis_max=dmax)
+        c = cuboid_from_disparity_range(w, h, dmin, dmax, num_labels=m)
+        depth, valid, oor, off, coll = o.ground_truth_to_depth(
+            sc.gt_image, sc.gt_scale, c.g_min, c.y_min, c.d_min, c.y_extent, c.g_extent, m, c.offset1, c.offset2,
+            c.offset3, c.lw_offset, c.rw_offset, c.h_offset)
+        assert sha(depth) == g["depth"] and sha(valid.astype(np.uint8)) == g["valid"]
+        assert (oor, off, coll) == (g["out_of_range"], g["off_grid"], g["collisions"])
+    # the reference's hand case (test_evalreport.py:34-47)
+    tot, ev, hist = o.error_count([[3, 7, 4], [1, 2, 20]], [[3, 5, 0], [2, 2, 9]],
+                                  [[True, True, False], [True, True, True]])
+    assert (tot, ev) == (14, 5) and hist[0] == 2 and hist[1] == 1 and hist[2] == 1 and hist[9] == 1
