@@ -53,6 +53,18 @@ sc, cub, gt, _ = gt_record(0, 384, 288, 10, 28, 16)
 vol = sad_volume(sc.left, sc.right, cub)
 res = solve_exact(vol, EnergyParams(14, 1023))
 out["c1_exact_error"] = {"labeling": sha(res.labeling.astype(np.int32)), **report(error_count(res.labeling, gt))}
+# disparity images (imaging.py:211-246): the C1 exact labeling, and a random labeling at an explicit scale
+import tempfile  # noqa: E402
+from gazecut.imaging import write_disparity_image  # noqa: E402
+with tempfile.TemporaryDirectory() as td:
+    p = Path(td) / "d.pgm"
+    scale = write_disparity_image(res.labeling, cub, p, 384, 288, comments=("gazecut exact", "penalty 14"))
+    out["disparity_images"] = [{"case": "c1_exact", "scale": scale, "sha": sha(np.frombuffer(p.read_bytes(), np.uint8))}]
+    c = cuboid_from_disparity_range(64, 12, 3, 13)
+    lab = np.random.default_rng(2).integers(0, c.num_labels, c.site_shape).astype(np.int32)
+    scale = write_disparity_image(lab, c, p, 64, 12, scale=7)
+    out["disparity_images"].append({"case": "random64x12", "scale": scale,
+                                    "sha": sha(np.frombuffer(p.read_bytes(), np.uint8))})
 # penalty sweeps: a small synthetic scene, and the reference test's random scene (test_evalreport.py:95-101)
 sc, cub, gt, _ = gt_record(3, 96, 64, 2, 13, 8)
 vol = sad_volume(sc.left, sc.right, cub)

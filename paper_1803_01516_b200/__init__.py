@@ -53,7 +53,20 @@ from .maxflow import (
     solve_exact_bands,
     source_side,
 )
-from .imaging import GroundTruthDepth, ground_truth_to_depth
+from .imaging import (
+    FileFormatError,
+    GroundTruthDepth,
+    disparity_of_labeling,
+    ground_truth_to_depth,
+    load_pgm,
+    load_ppm,
+    read_labeling,
+    render_disparity_device,
+    write_disparity_image,
+    write_labeling,
+    write_pgm,
+    write_ppm,
+)
 from .pairs import PairSolver, solve_pairs
 from .synthetic import SyntheticScene, make_scene
 
@@ -62,6 +75,8 @@ __version__ = "0.1.0"
 __all__ = [
     "HISTOGRAM_TAIL", "ErrorReport", "SweepRecord", "GroundTruthDepth", "best_penalty", "error_count",
     "error_count_device", "error_from_histogram", "ground_truth_to_depth", "sweep_penalty",
+    "FileFormatError", "disparity_of_labeling", "load_pgm", "load_ppm", "read_labeling",
+    "render_disparity_device", "write_disparity_image", "write_labeling", "write_pgm", "write_ppm",
     "CuboidSpec", "CutResult", "EnergyParams", "FlowNetwork", "GazeDepthCoord", "InternalConsistencyError",
     "PairSolver", "SyntheticScene", "UNCUTTABLE", "WhsCoord", "build_network", "coarsen",
     "cross_from_pixels", "cuboid_from_disparity_range", "cuboid_with_offsets", "disparity_from_whs",

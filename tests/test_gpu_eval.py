@@ -117,3 +117,26 @@ def test_sweep_penalty_c1_fifteen_penalties(gz):
     energies = [r.energy for r in recs]
     assert energies == sorted(energies)
     print("C1 sweep best penalty", gz.best_penalty(recs), "wall per solve", recs[0].wall_s)
+
+
+def test_disparity_images_byte_identical_to_reference(gz, tmp_path):
+    """imaging.py:211-246 through the device raster (gz_render_disparity)."""
+    want = {d["case"]: d for d in E["disparity_images"]}
+    sc, cub, gt = _scene_gt(gz, 0, 384, 288, 10, 28, 16)
+    r = gz.solve_exact(gz.sad_volume(sc.left, sc.right, cub), gz.EnergyParams(14, 1023))
+    p = tmp_path / "d.pgm"
+    scale = gz.write_disparity_image(r.labeling, cub, p, 384, 288, comments=("gazecut exact", "penalty 14"))
+    assert scale == want["c1_exact"]["scale"]
+    assert sha(np.frombuffer(p.read_bytes(), np.uint8)) == want["c1_exact"]["sha"]
+    c = gz.cuboid_from_disparity_range(64, 12, 3, 13)
+    lab = np.random.default_rng(2).integers(0, c.num_labels, c.site_shape).astype(np.int32)
+    assert gz.write_disparity_image(lab, c, p, 64, 12, scale=7) == 7
+    assert sha(np.frombuffer(p.read_bytes(), np.uint8)) == want["random64x12"]["sha"]
+    # ground-truth round trip (test_imaging.py:78-94): written image -> depth numbers
+    s2 = gz.write_disparity_image(lab, c, p, 64, 12)
+    g2 = gz.ground_truth_to_depth(gz.load_pgm(p), s2, c)
+    assert g2.num_valid > 0.5 * c.num_sites and g2.out_of_range == 0
+    assert np.array_equal(g2.depth[g2.valid], lab[g2.valid])
+    with pytest.raises(ValueError):
+        gz.write_disparity_image(np.zeros(gz.cuboid_from_disparity_range(64, 4, 1, 31).site_shape, np.int32),
+                                 gz.cuboid_from_disparity_range(64, 4, 1, 31), p, 64, 4, scale=100)
