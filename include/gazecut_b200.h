@@ -161,6 +161,13 @@ int gz_ground_truth_to_depth(const uint8_t *gt, int32_t img_h, int32_t img_w, in
 int gz_error_count(const int32_t *labels, int32_t batch, const int32_t *depth, const uint8_t *valid, int32_t rows,
                    int32_t cols, int32_t tail, int64_t *out, void *stream);
 
+/* imaging.py:211-246 write_disparity_image's raster: labels (rows, cols) int32
+ * -> image_out (img_h, img_w) uint8, site pixel x = g + d painted with
+ * dis * scale (nearer wins, uncovered pixels 0).  scratch: img_h * img_w int32.
+ * The caller checks scale * max disparity <= 255.  Device pointers. */
+int gz_render_disparity(const int32_t *labels, const gz_gaze *gaze, int32_t img_w, int32_t img_h, int32_t scale,
+                        int32_t *scratch, uint8_t *image_out, void *stream);
+
 /* The solves of evalreport.py:88-126 sweep_penalty: one volume (rows, cols, m)
  * int32 on the device, n energy parameter sets, exact solves (up to 8 in
  * flight, each on 1/8 of the SMs).  labels_out: n x rows x cols int32 (device),
@@ -189,6 +196,9 @@ int gz_thin_skin(const int32_t *coarse_labels, int32_t crows, int32_t ccols, int
  *   GZ_KTAIL, GZ_TAIL_AFTER   pulses per sweep from sweep GZ_TAIL_AFTER on (max(K, 96), 4)
  *   GZ_TAIL_MODE     0 disables the single-CTA tail mode (1)
  *   GZ_ASYNC_L       > 0: asynchronous pulses, iterations per team barrier (0)
+ *   GZ_WORKLIST      pulse worklists instead of per-pulse scans: 1 on, 0 off (auto: on for
+ *                    concurrent solves and for scans of >= 16 rounds per warp)
+ *   GZ_BAND_SPIN_MS  row bands: abort a team barrier wait after this long (30000)
  *   GZ_WATCHDOG_MS   device watchdog (20 s + 1 s per 2 M nodes)
  *   GZ_TRACE         1: per-sweep device trace, 2: per-pulse trace to stderr
  */

@@ -99,6 +99,8 @@ def lib():
                                              _vp, _vp, _i32, _vp, _vp, C.POINTER(Stats)]
         L.gz_ground_truth_to_depth.restype = C.c_int
         L.gz_ground_truth_to_depth.argtypes = [_vp, _i32, _i32, _i32, C.POINTER(Gaze), _vp, _vp, _vp, _vp]
+        L.gz_render_disparity.restype = C.c_int
+        L.gz_render_disparity.argtypes = [_vp, C.POINTER(Gaze), _i32, _i32, _i32, _vp, _vp, _vp]
         L.gz_error_count.restype = C.c_int
         L.gz_error_count.argtypes = [_vp, _i32, _vp, _vp, _i32, _i32, _i32, _vp, _vp]
         L.gz_solve_volume_batch.restype = C.c_int
@@ -133,6 +135,6 @@ def check(status: int, where: str) -> None:
 EXPORTED = (
     "gz_workspace_bytes", "gz_sad_volume", "gz_solve_volume", "gz_solve_pairs",
     "gz_solve_pairs_host", "gz_solve_volume_banded", "gz_ground_truth_to_depth",
-    "gz_error_count", "gz_solve_volume_batch", "gz_total_energy", "gz_coarsen", "gz_thin_skin",
+    "gz_error_count", "gz_render_disparity", "gz_solve_volume_batch", "gz_total_energy", "gz_coarsen", "gz_thin_skin",
     "gz_status_string", "gz_build_info",
 )

@@ -139,8 +139,9 @@ __device__ __forceinline__ int dn_of(const Lane<LP, R, WIN, RW> &L, int v, const
     return r;
 }
 
-// Shared-memory worklist of the single-CTA tail mode (gz_tilesolve.cuh): the
-// groups a pulse leaves active and every group it pushes into.
+// Worklist of the groups a pulse leaves active and every group it pushes into:
+// shared memory in the single-CTA tail mode, global memory for the team's
+// pulse worklists (gz_tilesolve.cuh).
 struct TailQ {
     int *q;
     unsigned *n;

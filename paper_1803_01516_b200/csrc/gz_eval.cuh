@@ -83,9 +83,42 @@ __global__ void k_error_count(const int32_t *__restrict__ lab, const int32_t *__
         if (s_h[i]) atomicAdd(&out[(size_t)b * (tail + 3) + i], s_h[i]);
 }
 
+// imaging.py:228-246 write_disparity_image: each site paints its right-image
+// pixel x = g + d with dis * scale, the nearer (larger disparity) wins.
+__global__ void k_render_disparity(const int32_t *__restrict__ lab, gz_gaze g, int img_w, int img_h, int scale,
+                                   int32_t *img) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= g.rows * g.cols) return;
+    const int yy = c / g.cols, gg = c - yy * g.cols;
+    const long long d = (long long)g.d_min + lab[c];
+    const long long dis = (long long)(img_w - 1) - 2 * d;
+    const long long x = (long long)g.g_min + gg + d, y = (long long)g.y_min + yy;
+    if (x < 0 || x >= img_w || y < 0 || y >= img_h) return;
+    atomicMax(&img[y * img_w + x], (int32_t)(dis * scale));
+}
+
+__global__ void k_i32_to_u8(const int32_t *__restrict__ src, uint8_t *dst, long long n) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = (uint8_t)src[i];
+}
+
 }  // namespace
 
 extern "C" {
+
+int gz_render_disparity(const int32_t *labels, const gz_gaze *gaze, int32_t img_w, int32_t img_h, int32_t scale,
+                        int32_t *scratch, uint8_t *image_out, void *stream) {
+    if (!labels || !gaze || !scratch || !image_out || img_w < 1 || img_h < 1 || scale < 1) return GZ_ERR_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    const long long n = (long long)img_w * img_h;
+    const int P = gaze->rows * gaze->cols;
+    CK(cudaMemsetAsync(scratch, 0, (size_t)n * 4, s));
+    k_render_disparity<<<(P + 255) / 256, 256, 0, s>>>(labels, *gaze, img_w, img_h, scale, scratch);
+    k_i32_to_u8<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(scratch, image_out, n);
+    CK(cudaGetLastError());
+    return GZ_OK;
+}
+
 
 int gz_ground_truth_to_depth(const uint8_t *gt, int32_t img_h, int32_t img_w, int32_t scale, const gz_gaze *gaze,
                              int32_t *depth_out, uint8_t *valid_out, int64_t *counts_out, void *stream) {

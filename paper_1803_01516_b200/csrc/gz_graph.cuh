@@ -60,6 +60,7 @@ struct Prob {
     int k_tail, tail_after;   // v4: pulses per sweep from sweep `tail_after` on (0 = K)
     int tail_mode;            // v4: hand nearly empty pulse phases to one CTA
     int async_l;              // v4: > 0 = asynchronous pulses, this many iterations per team barrier
+    int worklist;             // v4 exact: later pulses of a sweep consume a global worklist (1 on, 0 off, -1 auto)
     int bfs_adapt;            // v4: double the BFS early-stop depth when excess lies only beyond it
     int bfs_cap;         // lateral relaxations per non-final global relabel (0 = exact)
     int max_sweeps;      // honoured when capped
@@ -99,9 +100,10 @@ enum Ctr : int {
     CTR_TRACE = 35,     // debug trace accumulator (GZ_TRACE=2)
     CTR_TQN = 36,       // tail-mode global worklist length
     CTR_ABORT = 37,     // multi-launch (row-band) team gave up waiting at a barrier
+    CTR_WLN0 = 40,      // 4 rotating pulse-worklist lengths (v4 exact, gz_tilesolve.cuh)
     CTR_UPDATES = 30,   // node updates performed by pulses (v4)
     CTR_BAR0 = 32,      // 3 rotating team-barrier words (v4)
-    CTR_COUNT = 40
+    CTR_COUNT = 48
 };
 
 __host__ __device__ inline size_t plane_elems(int M, int P) { return (size_t)M * (size_t)P; }

@@ -1002,6 +1002,8 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
         p.tail_mode = tmode ? atoi(tmode) : 1;
         const char *al = getenv("GZ_ASYNC_L");
         p.async_l = al ? atoi(al) : 0;
+        const char *wl = getenv("GZ_WORKLIST");
+        p.worklist = wl ? atoi(wl) : -1;   // -1: auto (gz_tilesolve.cuh)
     }
     if (!v1 && p.bfs_cap < 0) p.bfs_cap = 0;            // exhaustive BFS every sweep
     const void *kern = nullptr;

@@ -287,9 +287,10 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
     __shared__ unsigned s_f3[3], s_r3[3], s_qn[2];
     __shared__ int s_q[BLOCK];   // per-round pool of active groups (<= 32 per warp)
     __shared__ unsigned s_tn[2];  // tail-mode worklist lengths
+    __shared__ unsigned s_wl[2];  // groups this CTA took from the pulse worklist (alternating)
     extern __shared__ uint32_t s_dyn[];
     if (threadIdx.x < 3) { s_f3[threadIdx.x] = 0u; s_r3[threadIdx.x] = 0u; }
-    if (threadIdx.x < 2) s_qn[threadIdx.x] = 0u;
+    if (threadIdx.x < 2) { s_qn[threadIdx.x] = 0u; s_wl[threadIdx.x] = 0u; }
     int qround = 0;
     __syncthreads();
     int phase = 0;
@@ -328,6 +329,24 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
     const int tail_cap = min(4096, ((int)(smem_bytes(OCC) / 4) - tail_bw) / 2);
     const bool tail_ok = tail_cap >= 256 && p.tail_mode;
     long long updates = 0;   // groups processed by pulses (x CPW x LP nodes)
+    // Pulse worklists (exact solves, one band): the first pulse of a sweep scans
+    // every group's active / inbox words; each later pulse consumes the list the
+    // previous one filled (the groups it left active and every group it pushed
+    // into) instead of scanning all groups.  Four lists rotate through planes
+    // that are idle during pulses (F0, F1, V, RL: list k is filled in pulse k-1,
+    // consumed in k, its claim bits cleared in k+1, its length reset in k+2);
+    // duplicates are dropped by claim bitmaps (two, alternating, in R0).  A list
+    // that overflowed falls back to the scan.  Auto (p.worklist < 0): on when a
+    // scan takes many rounds per warp (C3q 1.82 -> 1.59 s) and for the
+    // concurrent occupancy-2 instance (bench +2.5%); off for lone solves whose
+    // scan is one or a few rounds (C1 / C2 lone: the scan is 6-25% faster).
+    const bool wl_on = (p.worklist > 0 || (p.worklist < 0 && (OCC == 2 || giter >= 16 * 32))) && !p.capped &&
+                       p.async_l == 0 && g.nb == (int)gridDim.x;
+    const int wl_cap = nwords;
+    const int wl_bw = (ngroups + 31) / 32;
+    int *wl_list[4] = {(int *)b.F0, (int *)b.F1, (int *)b.V, (int *)b.RL};
+    uint32_t *wl_bits[2] = {(uint32_t *)b.R0, (uint32_t *)b.R0 + wl_bw};
+    unsigned *wl_n = (unsigned *)(p.ctr + CTR_WLN0);   // 4 x 32-bit counters in two ctr words
 
     // Scan the warps' interleaved groups (group it0+lane of every warp, 32 per
     // round), pool the ones whose word(s) in W1 | W2 are nonzero in shared memory,
@@ -476,6 +495,11 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
             b.A[w] = Vin[w] & b.EX[w];
             if (p.capped) b.RL[w] = 0u;   // (the BFS used RL as a visited buffer)
         }
+        if (wl_on) {
+            for (int i = ttid; i < 2 * wl_bw; i += tstride) wl_bits[0][i] = 0u;
+            if (threadIdx.x == 0 && tm.rank == 0)
+                for (int i = 0; i < 4; ++i) wl_n[i] = 0u;
+        }
         TEAM_SYNC();
         unsigned long long t_pulse = p.trace > 1 ? gz2::gtimer() : 0ull;
         // pulses this sweep: K, or K_tail once the dense opening sweeps are over
@@ -516,6 +540,45 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
                 for (int ai = 0; ai < p.async_l; ++ai) {
                     FOR_ACTIVE_GROUPS(b.A, a.IN0, updates, cta_groups, pulse_async)
                 }
+            } else if (wl_on) {
+                const int k4 = pulse & 3;
+                const gz3::TailQ nq{wl_list[(k4 + 1) & 3], wl_n + ((k4 + 1) & 3), wl_cap};
+                auto pulse_wl = [&](int cb, int sg) {
+                    gz3::w_pulse<LP, R, WIN, false, false, RW>(p, a, b, cb, CPW, sg, parity, flow, pushes, relabels,
+                                                               b.IN, &nq);
+                };
+                const unsigned n_cur = *(volatile unsigned *)(wl_n + k4);
+                if (pulse == 0 || n_cur > (unsigned)wl_cap) {
+                    FOR_ACTIVE_GROUPS(b.A, IN_prev, updates, cta_groups, pulse_wl)
+                } else {
+                    const int *lst = wl_list[k4];
+                    uint32_t *bits = wl_bits[pulse & 1];
+                    unsigned mine = 0;
+                    for (int q = gwid; q < (int)n_cur; q += gnw) {
+                        const int gg = __ldcg(lst + q);
+                        unsigned old = 0u;
+                        if (lane == 0) old = atomicOr(&bits[gg >> 5], 1u << (gg & 31));
+                        old = __shfl_sync(FULL, old, 0);
+                        if ((old >> (gg & 31)) & 1u) continue;   // already taken this pulse
+                        pulse_wl(LP == 16 ? 2 * gg : gg % p.P, LP == 16 ? 0 : gg / p.P);
+                        ++mine;
+                    }
+                    updates += mine;
+                    if (lane == 0 && mine) atomicAdd(&s_wl[pulse & 1], mine);
+                    __syncthreads();
+                    cta_groups += (int)s_wl[pulse & 1];
+                    if (threadIdx.x == 0) s_wl[(pulse + 1) & 1] = 0u;
+                }
+                // claim bits of the list consumed in the previous pulse
+                if (pulse >= 1) {
+                    const unsigned n_prev = *(volatile unsigned *)(wl_n + ((k4 + 3) & 3));
+                    if (n_prev <= (unsigned)wl_cap) {
+                        const int *lq = wl_list[(k4 + 3) & 3];
+                        uint32_t *bq = wl_bits[(pulse + 1) & 1];
+                        for (int q = ttid; q < (int)n_prev; q += tstride) bq[__ldcg(lq + q) >> 5] = 0u;
+                    }
+                }
+                if (threadIdx.x == 0 && tm.rank == 0) wl_n[(k4 + 2) & 3] = 0u;   // refilled from pulse + 1 on
             } else {
                 FOR_ACTIVE_GROUPS(b.A, IN_prev, updates, cta_groups, pulse_fn)
             }

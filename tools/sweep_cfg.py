@@ -19,7 +19,10 @@ vol = gz.sad_volume_device(sc.left, sc.right, cub)
 net = gz.build_network(vol, gz.EnergyParams(14, 1023))
 ref = None
 for H, cap, K in itertools.product(Hs, caps, Ks):
-    os.environ["GZ_BFS_H"] = str(H)
+    if H > 0:
+        os.environ["GZ_BFS_H"] = str(H)
+    else:   # 0: the library's residency-based default
+        os.environ.pop("GZ_BFS_H", None)
     try:
         lab, st = run(net, K, cap)
     except Exception as ex:  # noqa
