@@ -993,6 +993,8 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
     // hop, so the GPU sweep runs 2m pulses (24-label ladder: converges inside the
     // 8-sweep cap at b=3, tools/l2_quality.py)
     if (p.capped && 2 * m > p.K) p.K = 2 * m;
+    if (p.capped)
+        if (const char *ck = getenv("GZ_CAPPED_K")) p.K = atoi(ck) > 0 ? atoi(ck) : p.K;   // tuning override
     if (which == 4 && !p.capped) {   // tail sweeps: few active chains, pulses are cheap next to a global relabel
         const char *kt = getenv("GZ_KTAIL"), *ta = getenv("GZ_TAIL_AFTER");
         // measured (tools/bench_tune.py with adaptive relabels): 64 pulses from the fifth sweep on

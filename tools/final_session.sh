@@ -7,9 +7,9 @@ nvidia-smi > gpurun_out/nvsmi_$tag.txt 2>&1
 timeout 1200 python -m pytest tests -m gpu -q -s > gpurun_out/pytest_gpu_$tag.log 2>&1; echo "pytest rc $?" >> gpurun_out/pytest_gpu_$tag.log
 timeout 600 python bench.py > gpurun_out/bench_$tag.json 2> gpurun_out/bench_$tag.err
 timeout 300 python bench.py --impl reference --steps 1 --warmup 1 > gpurun_out/bench_ref_$tag.json 2> gpurun_out/bench_ref_$tag.err
-for c in 6 8; do GZ_PAIR_CONC=$c timeout 300 python bench.py --no-cpu-baseline > gpurun_out/bench_conc${c}_$tag.json 2>/dev/null; done
 timeout 300 python tools/paper_table.py > gpurun_out/paper_table_$tag.txt 2>&1
 timeout 200 python tools/big_configs.py C2 > gpurun_out/c2_$tag.txt 2>&1
+(cd tools && timeout 300 python hier_breakdown.py) > gpurun_out/hier_$tag.txt 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$tag.csv \
     python bench.py --steps 1 --warmup 3 --pairs 16 --no-cpu-baseline > gpurun_out/ncu_launch_$tag.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gz_tilesolve -s 48 -c 1 \
