@@ -35,12 +35,16 @@ from .geometry import (
 from .evalreport import (
     HISTOGRAM_TAIL,
     ErrorReport,
+    MethodRow,
     SweepRecord,
     best_penalty,
+    compare_methods,
     error_count,
     error_count_device,
     error_from_histogram,
     sweep_penalty,
+    write_compare_csv,
+    write_sweep_csv,
 )
 from .hierarchy import coarsen, solve_level1, solve_level2, thin_skin
 from .maxflow import (
@@ -73,7 +77,7 @@ from .synthetic import SyntheticScene, make_scene
 __version__ = "0.1.0"
 
 __all__ = [
-    "HISTOGRAM_TAIL", "ErrorReport", "SweepRecord", "GroundTruthDepth", "best_penalty", "error_count",
+    "HISTOGRAM_TAIL", "ErrorReport", "MethodRow", "compare_methods", "write_compare_csv", "write_sweep_csv", "SweepRecord", "GroundTruthDepth", "best_penalty", "error_count",
     "error_count_device", "error_from_histogram", "ground_truth_to_depth", "sweep_penalty",
     "FileFormatError", "disparity_of_labeling", "load_pgm", "load_ppm", "read_labeling",
     "render_disparity_device", "write_disparity_image", "write_labeling", "write_pgm", "write_ppm",

@@ -3,15 +3,17 @@ of the reference).
 
 ``error_count`` runs gz_error_count; ``sweep_penalty`` solves every penalty of
 the sweep with gz_solve_volume_batch (up to 8 exact solves in flight) and
-counts errors on the device, so no labeling makes a host round trip.  CSV
-writers and method comparisons are host-side reporting, out of scope."""
+counts errors on the device, so no labeling makes a host round trip.
+``compare_methods`` and the CSV writers are the reference's reporting
+callers, kept so experiment scripts switch over unchanged."""
 
 from __future__ import annotations
 
+import csv
 import ctypes as C
 import time
 from dataclasses import dataclass
-from typing import Sequence
+from typing import Optional, Sequence
 
 import numpy as np
 import torch
@@ -148,3 +150,87 @@ def sweep_penalty(volume, gt: GroundTruthDepth, penalties: Sequence[int], inhibi
 def best_penalty(records: Sequence[SweepRecord]) -> int:
     """evalreport.py:129-132: penalty of the smallest error (first on ties)."""
     return min(records, key=lambda r: (r.error, r.penalty)).penalty
+
+
+@dataclass
+class MethodRow:
+    """evalreport.py:135-145: one (level, block) configuration's outcome."""
+
+    level: int
+    block: int
+    energy: int
+    error: Optional[int]
+    exact_fraction: Optional[float]
+    wall_s: float
+    nodes: int
+    converged: bool = True
+
+
+def compare_methods(volume, params: EnergyParams, configs: Sequence[tuple[int, int]],
+                    gt: Optional[GroundTruthDepth] = None, skin_radius: int = 1, max_sweeps: Optional[int] = None,
+                    progress=None) -> list[MethodRow]:
+    """evalreport.py:148-186: run (level, block) configurations on one volume
+    (level 0 exact, 1 and 2 the hierarchy); errors counted on the device."""
+    from .hierarchy import solve_level1, solve_level2
+    from .maxflow import solve_exact
+    vol = _dev.as_device_i32(volume, "volume")
+    out = []
+    for level, block in configs:
+        if level not in (0, 1, 2):
+            raise ValueError(f"unknown level {level} (0, 1 or 2)")
+        t0 = time.perf_counter()
+        if level == 0:
+            res = solve_exact(vol, params)
+        elif level == 1:
+            res = solve_level1(vol, params, block, skin_radius=skin_radius)
+        else:
+            extra = {} if max_sweeps is None else {"max_sweeps": max_sweeps}
+            res = solve_level2(vol, params, block, skin_radius=skin_radius, **extra)
+        wall = time.perf_counter() - t0
+        rep = error_count(res.labeling, gt) if gt is not None else None
+        out.append(MethodRow(level=level, block=block, energy=res.energy,
+                             error=None if rep is None else rep.total_error,
+                             exact_fraction=None if rep is None else rep.exact_fraction, wall_s=wall,
+                             nodes=int(res.stats.get("nodes", 0)), converged=bool(res.stats.get("converged", True))))
+        if progress:
+            tail = "" if rep is None else f" error {rep.total_error}"
+            print(f"level {level} block {block}: energy {res.energy}{tail}", file=progress)
+    return out
+
+
+def _csv_target(path_or_file):
+    """(stream, close?) for a path or an already open text stream."""
+    if hasattr(path_or_file, "write"):
+        return path_or_file, False
+    return open(path_or_file, "w", newline=""), True
+
+
+def _write_csv(path_or_file, comments, header, rows) -> None:
+    f, close = _csv_target(path_or_file)
+    try:
+        for c in comments:
+            f.write(f"# {c}\n")
+        w = csv.writer(f)
+        w.writerow(header)
+        w.writerows(rows)
+    finally:
+        if close:
+            f.close()
+
+
+def write_sweep_csv(path, records: Sequence[SweepRecord], comments=(), timings=False) -> None:
+    """evalreport.py:197-210: penalty,energy,flow,error,exact_fraction[,wall_s]."""
+    header = ["penalty", "energy", "flow", "error", "exact_fraction"] + (["wall_s"] if timings else [])
+    rows = [[r.penalty, r.energy, r.flow, r.error, f"{r.exact_fraction:.6f}"] + ([f"{r.wall_s:.3f}"] if timings else [])
+            for r in records]
+    _write_csv(path, comments, header, rows)
+
+
+def write_compare_csv(path, rows: Sequence[MethodRow], comments=(), timings=False) -> None:
+    """evalreport.py:213-233: level,block,energy,error,exact_fraction,nodes,converged[,wall_s]."""
+    header = ["level", "block", "energy", "error", "exact_fraction", "nodes", "converged"] + \
+        (["wall_s"] if timings else [])
+    body = [[r.level, r.block, r.energy, "" if r.error is None else r.error,
+             "" if r.exact_fraction is None else f"{r.exact_fraction:.6f}", r.nodes, int(r.converged)] +
+            ([f"{r.wall_s:.3f}"] if timings else []) for r in rows]
+    _write_csv(path, comments, header, body)

@@ -140,3 +140,16 @@ def test_disparity_images_byte_identical_to_reference(gz, tmp_path):
     with pytest.raises(ValueError):
         gz.write_disparity_image(np.zeros(gz.cuboid_from_disparity_range(64, 4, 1, 31).site_shape, np.int32),
                                  gz.cuboid_from_disparity_range(64, 4, 1, 31), p, 64, 4, scale=100)
+
+
+def test_compare_methods_ladder(gz):
+    """evalreport.py:148-186 on the 24-label ladder: the reference's recorded
+    energies (pkg/test_output.txt:24) for exact / l1b2 / l1b3, e0 <= e1 <= e2."""
+    sc, cub, gt = _scene_gt(gz, 0, 384, 288, 10, 28, 24)
+    vol = gz.sad_volume(sc.left, sc.right, cub)
+    rows = gz.compare_methods(vol, gz.EnergyParams(14, 1023), [(0, 1), (1, 2), (1, 3), (2, 3)], gt=gt)
+    assert [r.energy for r in rows[:3]] == [778554, 785090, 790627]
+    assert rows[0].energy <= rows[1].energy and rows[2].energy <= rows[3].energy
+    assert all(r.error is not None and r.nodes > 0 for r in rows)
+    with pytest.raises(ValueError):
+        gz.compare_methods(vol, gz.EnergyParams(14, 1023), [(3, 1)])

@@ -69,3 +69,27 @@ def test_disparity_of_labeling():
     assert (disparity_of_labeling(lab, c) == 383 - 2 * c.d_min).all()
     lab[:] = c.num_labels - 1
     assert (disparity_of_labeling(lab, c) == 383 - 2 * c.d_max).all()
+
+
+def test_csv_writers(tmp_path):
+    """evalreport.py:197-233 formats (pkg/tests/test_evalreport.py:120-175)."""
+    import csv
+    import io
+
+    from paper_1803_01516_b200.evalreport import MethodRow, SweepRecord, write_compare_csv, write_sweep_csv
+    recs = [SweepRecord(3, 100, 90, 7, 0.5, 0.25), SweepRecord(6, 120, 110, 5, 0.75, 0.5)]
+    write_sweep_csv(tmp_path / "s.csv", recs, comments=("inhibit 30",), timings=True)
+    lines = (tmp_path / "s.csv").read_text().splitlines()
+    assert lines[0] == "# inhibit 30" and lines[1] == "penalty,energy,flow,error,exact_fraction,wall_s"
+    assert lines[2] == "3,100,90,7,0.500000,0.250"
+    buf = io.StringIO()
+    write_sweep_csv(buf, recs[:1], comments=("stream",))
+    assert buf.getvalue().splitlines() == ["# stream", "penalty,energy,flow,error,exact_fraction", "3,100,90,7,0.500000"]
+    rows = [MethodRow(0, 1, 50, 4, 0.25, 1.0, 30), MethodRow(2, 2, 55, None, None, 2.0, 12, False)]
+    write_compare_csv(tmp_path / "c.csv", rows, comments=("a", "b"))
+    lines = (tmp_path / "c.csv").read_text().splitlines()
+    assert lines[:2] == ["# a", "# b"]
+    parsed = list(csv.DictReader(lines[2:]))
+    assert parsed[0] == {"level": "0", "block": "1", "energy": "50", "error": "4", "exact_fraction": "0.250000",
+                         "nodes": "30", "converged": "1"}
+    assert parsed[1]["error"] == "" and parsed[1]["converged"] == "0"
