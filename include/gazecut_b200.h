@@ -191,6 +191,8 @@ int gz_thin_skin(const int32_t *coarse_labels, int32_t crows, int32_t ccols, int
 
 /* Runtime knobs (environment, read per solve; defaults are the measured best):
  *   GZ_PAIR_CONC     concurrent pair solves in gz_solve_pairs (8)
+ *   GZ_PAIR_DYNAMIC  0: static round-robin of pairs over the concurrent slots instead of
+ *                    handing the next pair to the first slot that finishes (1)
  *   GZ_OCC           2: occupancy-2 instance for m <= 16 (default when concurrent)
  *   GZ_BFS_H         BFS levels per temporally blocked round (8)
  *   GZ_KTAIL, GZ_TAIL_AFTER   pulses per sweep from sweep GZ_TAIL_AFTER on (max(K, 96), 4)

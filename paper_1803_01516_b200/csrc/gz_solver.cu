@@ -29,6 +29,8 @@
 #include <ctime>
 #include <unistd.h>
 
+#include <vector>
+
 #include "gazecut_b200.h"
 #include "gz_graph.cuh"
 
@@ -1308,8 +1310,7 @@ int gz_solve_pairs(const uint8_t *left, const uint8_t *right, int32_t batch, int
         for (int k = 0; k < conc; ++k) CK(cudaStreamWaitEvent(streams[k], fork, 0));
     }
     Pending *pend = new Pending[batch];
-    for (int b = 0; b < batch && rc == GZ_OK; ++b) {
-        const int k = b % conc;
+    auto enqueue = [&](int b, int k) -> int {   // data term + solve of pair b on slot k
         cudaStream_t sk = conc > 1 ? streams[k] : s;
         Workspace w = carve((uint8_t *)workspace + (size_t)k * one, rows, cols, m);
         if (which == 4)
@@ -1317,14 +1318,49 @@ int gz_solve_pairs(const uint8_t *left, const uint8_t *right, int32_t batch, int
                                                       lanes_for(m));
         else
             k_sad<1><<<(P + 127) / 128, 128, 0, sk>>>(left + b * img, right + b * img, img_w, channels, *cb, w.vol);
-        if (cudaGetLastError() != cudaSuccess) { rc = GZ_ERR_CUDA; break; }
-        rc = solve_launch(w, rows, cols, m, energy, sched, nullptr, nullptr, labels_out + (size_t)b * P, sk, 1 << 30,
-                          conc, pinned + (size_t)b * gz::CTR_COUNT, &pend[b]);
-        if (rc) break;
-        if (conc == 1) {   // one at a time: collect now (keeps the pinned slot reuse trivial)
-            if (cudaStreamSynchronize(s) != cudaSuccess) { rc = GZ_ERR_CUDA; break; }
-            rc = solve_finish(pend[b], stats_out ? stats_out + b : nullptr);
-            pend[b].e0 = nullptr;
+        if (cudaGetLastError() != cudaSuccess) return GZ_ERR_CUDA;
+        return solve_launch(w, rows, cols, m, energy, sched, nullptr, nullptr, labels_out + (size_t)b * P, sk, 1 << 30,
+                            conc, pinned + (size_t)b * gz::CTR_COUNT, &pend[b]);
+    };
+    const char *dy = getenv("GZ_PAIR_DYNAMIC");
+    if (conc > 1 && (!dy || atoi(dy))) {
+        // Dynamic dispatch: every slot holds at most two pairs (one running, one
+        // queued behind it); the host hands the next pair to the first slot whose
+        // oldest pair has finished.  Pair solve times vary by 2x, so a static
+        // round-robin of 8 pairs per slot left the step waiting on the slowest
+        // slot (step 149 ms against 124 ms of mean slot work, round 1).
+        std::vector<std::vector<int>> q(conc);
+        int next = 0;
+        for (int d = 0; d < 2; ++d)
+            for (int k = 0; k < conc && next < batch && rc == GZ_OK; ++k) {
+                rc = enqueue(next, k);
+                q[k].push_back(next++);
+            }
+        while (rc == GZ_OK) {
+            bool any = false;
+            for (int k = 0; k < conc && rc == GZ_OK; ++k) {
+                if (q[k].empty()) continue;
+                any = true;
+                const cudaError_t e = cudaEventQuery(pend[q[k].front()].e1);
+                if (e == cudaErrorNotReady) continue;
+                if (e != cudaSuccess) { rc = GZ_ERR_CUDA; break; }
+                q[k].erase(q[k].begin());
+                if (next < batch) {
+                    rc = enqueue(next, k);
+                    q[k].push_back(next++);
+                }
+            }
+            if (!any) break;
+        }
+    } else {
+        for (int b = 0; b < batch && rc == GZ_OK; ++b) {
+            rc = enqueue(b, b % conc);
+            if (rc) break;
+            if (conc == 1) {   // one at a time: collect now (keeps the pinned slot reuse trivial)
+                if (cudaStreamSynchronize(s) != cudaSuccess) { rc = GZ_ERR_CUDA; break; }
+                rc = solve_finish(pend[b], stats_out ? stats_out + b : nullptr);
+                pend[b].e0 = nullptr;
+            }
         }
     }
     if (conc > 1) {
