@@ -142,11 +142,37 @@ __device__ __forceinline__ int dn_of(const Lane<LP, R, WIN, RW> &L, int v, const
 // Worklist of the groups a pulse leaves active and every group it pushes into:
 // shared memory in the single-CTA tail mode, global memory for the team's
 // pulse worklists (gz_tilesolve.cuh).
+// Team worklists are split by row band: band j's list lives at list + nw c0(j)
+// (in its own band's memory) and its length at cnt[c0(j)].
+struct BandRoute {
+    int *list;
+    unsigned *cnt;
+    int ny, nbands, TY, G, Y, P, nw, lp16, sys;
+    __device__ __forceinline__ int c0(int j) const { return min(ny * j / nbands * TY, Y) * G; }
+    __device__ __forceinline__ int band_of(int grp) const {
+        const int site = lp16 ? min(2 * grp + 1, P - 1) : grp % P;   // a pair goes where its upper site is
+        const int ty = (site / G) / TY;
+        return ((ty + 1) * nbands + ny - 1) / ny - 1;
+    }
+};
+
 struct TailQ {
     int *q;
     unsigned *n;
     int cap;
+    const BandRoute *rt = nullptr;   // team worklist: route to the target group's band
     __device__ __forceinline__ void push(int grp) const {
+        if (rt && rt->nbands == 1) {   // one band: list and length at the plane bases
+            const unsigned k = atomicAdd(rt->cnt, 1u);
+            if ((int)k < rt->nw * rt->P) rt->list[k] = grp;
+            return;
+        }
+        if (rt) {
+            const int j = rt->band_of(grp), c0 = rt->c0(j), c1 = rt->c0(j + 1);
+            const unsigned k = rt->sys ? atomicAdd_system(rt->cnt + c0, 1u) : atomicAdd(rt->cnt + c0, 1u);
+            if ((int)k < rt->nw * (c1 - c0)) rt->list[(size_t)rt->nw * c0 + k] = grp;
+            return;
+        }
         const unsigned k = atomicAdd(n, 1u);
         if ((int)k < cap) q[k] = grp;
     }

@@ -100,10 +100,9 @@ enum Ctr : int {
     CTR_TRACE = 35,     // debug trace accumulator (GZ_TRACE=2)
     CTR_TQN = 36,       // tail-mode global worklist length
     CTR_ABORT = 37,     // multi-launch (row-band) team gave up waiting at a barrier
-    CTR_WLN0 = 40,      // 4 rotating pulse-worklist lengths (v4 exact, gz_tilesolve.cuh)
     CTR_UPDATES = 30,   // node updates performed by pulses (v4)
     CTR_BAR0 = 32,      // 3 rotating team-barrier words (v4)
-    CTR_COUNT = 48
+    CTR_COUNT = 40
 };
 
 __host__ __device__ inline size_t plane_elems(int M, int P) { return (size_t)M * (size_t)P; }

@@ -883,7 +883,7 @@ gz4::Geo tile_geo(int rows, int cols, int nb, int nw, int occ) {
     g.t0 = 0; g.t1 = g.ntiles;
     g.c0 = 0; g.c1 = rows * cols;
     g.gg0 = 0; g.gg1 = (rows * cols + 1) / 2;
-    g.sys = 0; g.spin_ms = 0;
+    g.sys = 0; g.spin_ms = 0; g.nbands = 1;
     return g;
 }
 
@@ -914,6 +914,7 @@ gz4::Geo band_geo(const gz4::Geo &g, int rows, int cols, int n, int k, int rank0
     b.rank0 = rank0;
     b.sys = multi_dev;
     b.spin_ms = n > 1 ? spin_ms : 0;
+    b.nbands = n;
     return b;
 }
 

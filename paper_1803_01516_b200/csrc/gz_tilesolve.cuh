@@ -60,6 +60,7 @@ struct Geo {
     int t0, t1, c0, c1;    // this band's tiles and sites
     int gg0, gg1;          // this band's site-pair groups (LP = 16)
     int sys;               // bands on several GPUs: system-scope fences in the team barrier
+    int nbands;            // bands of the team (1: one launch)
     int spin_ms;           // multi-launch team: abort a barrier wait after this long (0: never)
 };
 
@@ -340,13 +341,20 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
     // scan takes many rounds per warp (C3q 1.82 -> 1.59 s) and for the
     // concurrent occupancy-2 instance (bench +2.5%); off for lone solves whose
     // scan is one or a few rounds (C1 / C2 lone: the scan is 6-25% faster).
-    const bool wl_on = (p.worklist > 0 || (p.worklist < 0 && (OCC == 2 || giter >= 16 * 32))) && !p.capped &&
-                       p.async_l == 0 && g.nb == (int)gridDim.x;
-    const int wl_cap = nwords;
+    // With row bands every band keeps its own four lists (in its own sites' part of
+    // the planes) and lengths (R1, idle during pulses); pushes route to the band
+    // of the target group.  Auto leaves them off for row bands: C3q as two bands
+    // on one GPU took 2.61 s with band worklists against 2.09 s scanning (the
+    // routing arithmetic per push, round 1); GZ_WORKLIST=1 forces them on.
+    const bool wl_on = (p.worklist > 0 || (p.worklist < 0 && g.nbands == 1 && (OCC == 2 || giter >= 16 * 32))) &&
+                       !p.capped && p.async_l == 0;
+    const int wl_cap = NW * (g.c1 - g.c0);
     const int wl_bw = (ngroups + 31) / 32;
-    int *wl_list[4] = {(int *)b.F0, (int *)b.F1, (int *)b.V, (int *)b.RL};
+    int *wl_plane[4] = {(int *)b.F0, (int *)b.F1, (int *)b.V, (int *)b.RL};
+    const int *wl_list[4] = {wl_plane[0] + (size_t)NW * g.c0, wl_plane[1] + (size_t)NW * g.c0,
+                             wl_plane[2] + (size_t)NW * g.c0, wl_plane[3] + (size_t)NW * g.c0};
     uint32_t *wl_bits[2] = {(uint32_t *)b.R0, (uint32_t *)b.R0 + wl_bw};
-    unsigned *wl_n = (unsigned *)(p.ctr + CTR_WLN0);   // 4 x 32-bit counters in two ctr words
+    unsigned *wl_n = (unsigned *)b.R1 + g.c0;   // this band's 4 list lengths
 
     // Scan the warps' interleaved groups (group it0+lane of every warp, 32 per
     // round), pool the ones whose word(s) in W1 | W2 are nonzero in shared memory,
@@ -496,8 +504,8 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
             if (p.capped) b.RL[w] = 0u;   // (the BFS used RL as a visited buffer)
         }
         if (wl_on) {
-            for (int i = ttid; i < 2 * wl_bw; i += tstride) wl_bits[0][i] = 0u;
-            if (threadIdx.x == 0 && tm.rank == 0)
+            for (int i = tm.rank * blockDim.x + threadIdx.x; i < 2 * wl_bw; i += tm.nb * blockDim.x) wl_bits[0][i] = 0u;
+            if (threadIdx.x == 0 && blockIdx.x == 0)
                 for (int i = 0; i < 4; ++i) wl_n[i] = 0u;
         }
         TEAM_SYNC();
@@ -542,7 +550,9 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
                 }
             } else if (wl_on) {
                 const int k4 = pulse & 3;
-                const gz3::TailQ nq{wl_list[(k4 + 1) & 3], wl_n + ((k4 + 1) & 3), wl_cap};
+                const gz3::BandRoute rt{wl_plane[(k4 + 1) & 3], (unsigned *)b.R1 + ((k4 + 1) & 3), g.ny, g.nbands,
+                                        g.TY, p.G, p.Y, p.P, NW, LP == 16 ? 1 : 0, p.sys};
+                const gz3::TailQ nq{nullptr, nullptr, 0, &rt};
                 auto pulse_wl = [&](int cb, int sg) {
                     gz3::w_pulse<LP, R, WIN, false, false, RW>(p, a, b, cb, CPW, sg, parity, flow, pushes, relabels,
                                                                b.IN, &nq);
@@ -557,7 +567,7 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
                     for (int q = gwid; q < (int)n_cur; q += gnw) {
                         const int gg = __ldcg(lst + q);
                         unsigned old = 0u;
-                        if (lane == 0) old = atomicOr(&bits[gg >> 5], 1u << (gg & 31));
+                        if (lane == 0) old = gz_atomic_or(p, &bits[gg >> 5], 1u << (gg & 31));
                         old = __shfl_sync(FULL, old, 0);
                         if ((old >> (gg & 31)) & 1u) continue;   // already taken this pulse
                         pulse_wl(LP == 16 ? 2 * gg : gg % p.P, LP == 16 ? 0 : gg / p.P);
@@ -578,7 +588,7 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
                         for (int q = ttid; q < (int)n_prev; q += tstride) bq[__ldcg(lq + q) >> 5] = 0u;
                     }
                 }
-                if (threadIdx.x == 0 && tm.rank == 0) wl_n[(k4 + 2) & 3] = 0u;   // refilled from pulse + 1 on
+                if (threadIdx.x == 0 && blockIdx.x == 0) wl_n[(k4 + 2) & 3] = 0u;   // refilled from pulse + 1 on
             } else {
                 FOR_ACTIVE_GROUPS(b.A, IN_prev, updates, cta_groups, pulse_fn)
             }

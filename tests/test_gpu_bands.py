@@ -85,3 +85,17 @@ def test_band_argument_errors(gz):
         gz.solve_exact_bands(vol, gz.EnergyParams(14, 1023), devices=(0,) * 16)
     with pytest.raises(ValueError):
         gz.solve_exact_bands(vol, gz.EnergyParams(14, 1023), devices=(99,))
+
+
+@pytest.mark.parametrize("m", [16, 40])
+def test_band_worklists_forced(gz, monkeypatch, m):
+    """Band-routed pulse worklists (GZ_WORKLIST=1; auto leaves them off for
+    bands): every push goes to the list of the target group's band."""
+    rng = np.random.default_rng(500 + m)
+    vol = rng.integers(0, 300, size=(160, 200, m)).astype(np.int64)
+    p = gz.EnergyParams(14, 60)
+    one = gz.solve_exact(vol, p)
+    monkeypatch.setenv("GZ_WORKLIST", "1")
+    for nb in (1, 3):
+        r = gz.solve_exact_bands(vol, p, devices=(0,) * nb)
+        assert r.flow == one.flow and np.array_equal(r.labeling, one.labeling), (m, nb)
