@@ -1015,7 +1015,6 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
 #define GZ_PICK(W_, NW_, D_) if (win == W_ && NW == NW_ && det == D_) kern = (const void *)gz2::gz_bitsolve_kernel<W_, NW_, D_>;
 #define GZ_PICK_NW(NW_) GZ_PICK(false, NW_, false) GZ_PICK(false, NW_, true) GZ_PICK(true, NW_, false) GZ_PICK(true, NW_, true)
     const int LPn = lanes_for(m);
-    bool rel = false;   // window-relative instance (set below)
     // two CTAs per SM (64 registers, smaller BFS regions) for the m <= 16 instance
     // (spills cost ~12% on a lone solve; with concurrent pair solves the doubled
     // warp count wins ~12%: bench A/B, round 1)
@@ -1034,8 +1033,6 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
         if (win && max_width >= 0 && max_width <= 15 && (LPn == 32 || LPn == 64) && !getenv("GZ_NO_REL")) {
             kern = LPn == 32 ? (const void *)gz4::gz_tilesolve_kernel<16, 1, true, 1, 1>
                              : (const void *)gz4::gz_tilesolve_kernel<16, 1, true, 1, 2>;
-            rel = true;
-            (void)rel;
         }
     } else if (which == 2) {
         GZ_PICK_NW(1) GZ_PICK_NW(2) GZ_PICK_NW(4) GZ_PICK_NW(8)
