@@ -200,6 +200,8 @@ int gz_thin_skin(const int32_t *coarse_labels, int32_t crows, int32_t ccols, int
  *   GZ_ASYNC_L       > 0: asynchronous pulses, iterations per team barrier (0)
  *   GZ_WORKLIST      pulse worklists instead of per-pulse scans: 1 on, 0 off (auto: on for
  *                    concurrent solves and for scans of >= 16 rounds per warp)
+ *   GZ_WL_DEDUPE     0: keep every push in the pulse worklist (1: a push into an inbox word
+ *                    already set this pulse is not listed again)
  *   GZ_BAND_SPIN_MS  row bands: abort a team barrier wait after this long (30000)
  *   GZ_WATCHDOG_MS   device watchdog (20 s + 1 s per 2 M nodes)
  *   GZ_TRACE         1: per-sweep device trace, 2: per-pulse trace to stderr

@@ -161,6 +161,11 @@ struct TailQ {
     unsigned *n;
     int cap;
     const BandRoute *rt = nullptr;   // team worklist: route to the target group's band
+    // push-time dedupe (team worklists): a push whose inbox word was already
+    // nonzero this pulse skips the list -- the first push into that word listed
+    // the group (inbox words are zero at pulse start: the owner clears them when
+    // it is processed, and every group with inbox bits is listed or scanned)
+    int dedupe = 0;
     __device__ __forceinline__ void push(int grp) const {
         if (rt && rt->nbands == 1) {   // one band: list and length at the plane bases
             const unsigned k = atomicAdd(rt->cnt, 1u);
@@ -519,8 +524,8 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
                 flow += x_out;
             } else if (L.top_edge()) {   // into the next segment's first node
                 gz_atomic_add(p, &ein_cur[I + 1], x_out);
-                gz_atomic_or(p, &IN_cur[L.wi + P], 1u);
-                if (tq) tq->push(L.wi + P);
+                const uint32_t o_ = gz_atomic_or(p, &IN_cur[L.wi + P], 1u);
+                if (tq && !(o_ && tq->dedupe)) tq->push(L.wi + P);
             }
         }
     }
@@ -554,8 +559,8 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
         int site, pos;
         lateral_target(L, jj, site, pos);
         gz_atomic_add(p, &ein_cur[site * LPT + pos - 1], d);
-        gz_atomic_or(p, &IN_cur[((pos - 1) >> 5) * P + site], 1u << ((pos - 1) & 31));
-        if (tq) tq->push(LP == 16 ? site >> 1 : ((pos - 1) / LP) * P + site);
+        const uint32_t o_ = gz_atomic_or(p, &IN_cur[((pos - 1) >> 5) * P + site], 1u << ((pos - 1) & 31));
+        if (tq && !(o_ && tq->dedupe)) tq->push(LP == 16 ? site >> 1 : ((pos - 1) / LP) * P + site);
     }
     // chain-down pushes arrive at lane j-1 (adds to its excess and to its chain-up
     // residual); out of a segment's first lane they cross into the segment below
@@ -568,8 +573,8 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
     if (!RW && dn > 0 && L.bot_edge()) {
         gz_atomic_add(p, &a.cu[I - 1], dn);   // (the segment below applies its own cu change atomically too)
         gz_atomic_add(p, &ein_cur[I - 1], dn);
-        gz_atomic_or(p, &IN_cur[L.wi - P], 1u << (LP - 1));
-        if (tq) tq->push(L.wi - P);
+        const uint32_t o_ = gz_atomic_or(p, &IN_cur[L.wi - P], 1u << (LP - 1));
+        if (tq && !(o_ && tq->dedupe)) tq->push(L.wi - P);
     }
     // relabel a live node that could not push (deterministic mode: a later phase)
     int hnew = hu;

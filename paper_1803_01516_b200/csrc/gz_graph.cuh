@@ -60,6 +60,7 @@ struct Prob {
     int k_tail, tail_after;   // v4: pulses per sweep from sweep `tail_after` on (0 = K)
     int tail_mode;            // v4: hand nearly empty pulse phases to one CTA
     int async_l;              // v4: > 0 = asynchronous pulses, this many iterations per team barrier
+    int wl_dedupe;            // v4 exact: push-time dedupe of worklist entries (GZ_WL_DEDUPE)
     int worklist;             // v4 exact: later pulses of a sweep consume a global worklist (1 on, 0 off, -1 auto)
     int bfs_adapt;            // v4: double the BFS early-stop depth when excess lies only beyond it
     int bfs_cap;         // lateral relaxations per non-final global relabel (0 = exact)

@@ -552,7 +552,7 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
                 const int k4 = pulse & 3;
                 const gz3::BandRoute rt{wl_plane[(k4 + 1) & 3], (unsigned *)b.R1 + ((k4 + 1) & 3), g.ny, g.nbands,
                                         g.TY, p.G, p.Y, p.P, NW, LP == 16 ? 1 : 0, p.sys};
-                const gz3::TailQ nq{nullptr, nullptr, 0, &rt};
+                const gz3::TailQ nq{nullptr, nullptr, 0, &rt, p.wl_dedupe};
                 auto pulse_wl = [&](int cb, int sg) {
                     gz3::w_pulse<LP, R, WIN, false, false, RW>(p, a, b, cb, CPW, sg, parity, flow, pushes, relabels,
                                                                b.IN, &nq);
