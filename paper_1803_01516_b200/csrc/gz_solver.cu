@@ -1051,6 +1051,8 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
     int rc = coop_grid(kern, threads, &grid, dyn_smem);
     if (rc) return rc;
     if (conc > 1) grid = grid / conc > 0 ? grid / conc : 1;
+    if (conc == 1)   // tuning override: CTAs of a lone solve
+        if (const char *lg = getenv("GZ_LONE_GRID")) grid = atoi(lg) > 0 && atoi(lg) < grid ? atoi(lg) : grid;
     const int need = (p.P + 255) / 256;
     if (grid > need) grid = need < 1 ? 1 : need;
     gz4::Geo geo{};
