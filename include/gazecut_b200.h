@@ -75,8 +75,9 @@ typedef struct {
 #define GZ_SCHED_NO_WAVE 1
 #define GZ_SCHED_CAPPED 2
 #define GZ_SCHED_V1 4      /* force the v1 (column-relaxation) solver; debugging/comparison */
-#define GZ_SCHED_V2 8      /* force the v2 (bit-parallel, thread-per-chain) solver */
+#define GZ_SCHED_V2 8      /* retired v2 solver (deleted in round 2); accepted and ignored (v4 runs) */
 #define GZ_SCHED_V3 16     /* retired v3 solver; accepted and ignored (v4 runs) */
+#define GZ_SCHED_INIT_ONLY 32  /* stop after the solver's initialisation (graph export, gz_export_arcs) */
 
 /* maxflow.py:460-471 + 506-509 stats keys, plus device timings. */
 typedef struct {
@@ -84,6 +85,10 @@ typedef struct {
     int64_t labeling_energy;       /* energy.py:129-155 recomputed on device */
     int64_t node_updates;          /* node updates done by push/relabel pulses (v4; roofline units) */
     int32_t sweeps, converged, stranded_excess_nodes, bfs_passes, reach_passes, pulses;
+    int32_t bfs_h;                 /* BFS levels per temporally blocked round (v4): the capped level-2
+                                      schedule's early-stop granularity (oracle/gz_oracle.c restates it) */
+    int32_t excess_nodes;          /* nodes holding excess when the solve stopped (phase-1 leftover that
+                                      the reference's phase 2 would return to the source) */
     float ms_total;                /* device time of the solve (CUDA events) */
     float ms_phase[6];             /* in-kernel phase times: init, mask build, global relabel, pulses,
                                       extraction, energy/labels (v2 solver; 0 for v1) */
@@ -177,7 +182,9 @@ int gz_solve_volume_batch(const int32_t *vol, int32_t rows, int32_t cols, int32_
                           int32_t n, const gz_sched *sched, int32_t *labels_out, gz_stats *stats_out,
                           void *workspace, size_t workspace_bytes, void *stream);
 
-/* energy.py:129-155 total_energy on device.  Writes one int64 to energy_out (device). */
+/* energy.py:129-155 total_energy on device.  energy_out (device) must hold TWO
+ * int64: [0] the energy, [1] a hard-inhibit violation flag (1 when a hard
+ * inhibit is violated; the reference then reports UNCUTTABLE, energy.py:149-150). */
 int gz_total_energy(const int32_t *labels, const int32_t *vol, int32_t rows, int32_t cols, int32_t m,
                     const gz_energy *energy, int64_t *energy_out, void *stream);
 
@@ -206,6 +213,73 @@ int gz_thin_skin(const int32_t *coarse_labels, int32_t crows, int32_t ccols, int
  *   GZ_WATCHDOG_MS   device watchdog (20 s + 1 s per 2 M nodes)
  *   GZ_TRACE         1: per-sweep device trace, 2: per-pulse trace to stderr
  */
+
+/* ---- explicit networks (debug export, certificates, generic graphs) ---- */
+
+/* flownet.py:102-181 _emit / flownet.py:233-296 build_network, read back from
+ * the DEVICE graph: runs the solver's own initialisation (no presaturating
+ * wave) and enumerates the implicit graph's arc pairs in the reference's
+ * emission order, capacities taken from the initialised state planes.
+ * pair_u/v/cap/rcap: device int64[capacity] (tail, head, capacity, reverse
+ * capacity; node ids as flownet.py numbers them, source = n-2, sink = n-1), or
+ * all NULL to count only.  info (host int64[4]): [0] pairs, [1] the constant
+ * offset folded by the export, [2] nodes, [3] the constant offset of the
+ * device initialisation (the two must agree).  Exact pairs for m <= 256. */
+int gz_export_arcs(const int32_t *vol, int32_t rows, int32_t cols, int32_t m, const gz_energy *energy,
+                   const int32_t *lo, const int32_t *hi, int64_t *pair_u, int64_t *pair_v, int64_t *pair_cap,
+                   int64_t *pair_rcap, int64_t capacity, int64_t *info, void *workspace, size_t workspace_bytes,
+                   void *stream);
+
+/* One state plane of the last v4 solve run in `workspace` (m <= 256), as
+ * int32 (rows*cols, m-1), position t at column t-1: the certificate input
+ * (oracle/gz_certify.c).  Device pointers, stream-ordered. */
+enum gz_plane {
+    GZ_PLANE_CHAIN = 0,        /* residual of chain arc t -> t+1 (capacity vol[t]) */
+    GZ_PLANE_SAME_RIGHT = 1,   /* residual of (y,g,t) -> (y,g+1,t); reverse = 2*penalty - r */
+    GZ_PLANE_SAME_DOWN = 2,    /* residual of (y,g,t) -> (y+1,g,t) */
+    GZ_PLANE_DIAG_RIGHT = 3,   /* flow on (y,g,t) -> (y,g+1,t-1) (capacity inhibit) */
+    GZ_PLANE_DIAG_LEFT = 4,    /* flow on (y,g+1,t) -> (y,g,t-1), stored at (y,g) */
+    GZ_PLANE_DIAG_DOWN = 5,    /* flow on (y,g,t) -> (y+1,g,t-1) */
+    GZ_PLANE_DIAG_UP = 6,      /* flow on (y+1,g,t) -> (y,g,t-1), stored at (y,g) */
+    GZ_PLANE_EXCESS = 7,       /* excess (inboxes merged) */
+    GZ_PLANE_HEIGHT = 8        /* height of the last relabel */
+};
+int gz_export_state(const void *workspace, int32_t rows, int32_t cols, int32_t m, int32_t plane, int32_t *out,
+                    void *stream);
+
+/* maxflow.py:403-478 result counters of gz_maxflow_csr. */
+typedef struct {
+    int64_t flow, pushes, relabels, stranded_excess_nodes;
+    int32_t sweeps, converged, pulses;
+    float ms_total;
+} gz_csr_stats;
+
+/* Device workspace for gz_maxflow_csr on n_nodes nodes. */
+size_t gz_csr_workspace_bytes(int64_t n_nodes);
+
+/* maxflow.py:403-478 maxflow_push_relabel on an explicit CSR network
+ * (flownet.py:41-89 FlowNetwork arrays; flownet.py:325-353 network_from_arcs):
+ * source saturation, global relabeling (sink distance, n + source distance,
+ * 2n parked: maxflow.py:138-170) and rounds_per_sweep synchronous pulses per
+ * sweep until no active node remains (or max_sweeps >= 0 sweeps ran).  Both
+ * phases run, so `resid` (device int64, updated in place) ends as a maximum
+ * flow with no excess left, like the reference's.  side_out (device uint8[n],
+ * or NULL): maxflow.py:267-284 source side.  excess_out (device int64[n] or
+ * NULL).  Device pointers except stats_out (host). */
+int gz_maxflow_csr(int64_t n_nodes, int64_t source, int64_t sink, const int64_t *first_out, const int32_t *head,
+                   const int32_t *rev, int64_t *resid, int32_t rounds_per_sweep, int32_t max_sweeps,
+                   uint8_t *side_out, int64_t *excess_out, gz_csr_stats *stats_out, void *workspace,
+                   size_t workspace_bytes, void *stream);
+
+/* maxflow.py:287-304 _chain_presaturate on CSR arrays (device; sent_out is a
+ * device int64). */
+int gz_chain_presaturate_csr(const int32_t *rev, int64_t *resid, const int32_t *chain_arcs, const int64_t *chain_base,
+                             int64_t nsites, int64_t *sent_out, void *stream);
+
+/* maxflow.py:323-334 _conservation_violations on CSR arrays (device; bad_out
+ * is a device int64). */
+int gz_conservation_violations_csr(const int64_t *first_out, const int64_t *cap, const int64_t *resid, int64_t n_nodes,
+                                   int64_t source, int64_t sink, int64_t *bad_out, void *stream);
 
 /* Human-readable status. */
 const char *gz_status_string(int status);

@@ -25,7 +25,7 @@ GZ_ERR_BANDS = -8
 GZ_SCHED_NO_WAVE = 1
 GZ_SCHED_CAPPED = 2
 GZ_SCHED_V1 = 4
-GZ_SCHED_V2 = 8
+GZ_SCHED_V2 = 8   # retired (maps to the default v4 solver)
 GZ_SCHED_V3 = 16  # retired (maps to the default v4 solver)
 
 
@@ -55,7 +55,7 @@ class Stats(C.Structure):
                  "relabels", "labeling_energy", "node_updates")] + \
                [(n, C.c_int32) for n in
                 ("sweeps", "converged", "stranded_excess_nodes", "bfs_passes", "reach_passes",
-                 "pulses")] + \
+                 "pulses", "bfs_h", "excess_nodes")] + \
                [("ms_total", C.c_float), ("ms_phase", C.c_float * 6)]
 
 

@@ -14,7 +14,9 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
-SOURCES = [PKG / "csrc" / "gz_solver.cu"]
+# gz_solver.cu: host side, C ABI, small kernels; gz_k*.cu: the v4 solve-kernel
+# instances (the long compiles), built in parallel and linked into one library
+SOURCES = [PKG / "csrc" / n for n in ("gz_solver.cu", "gz_k16.cu", "gz_k32.cu", "gz_k32w.cu")]
 HEADERS = sorted((PKG / "csrc").glob("*.cuh")) + [ROOT / "include" / "gazecut_b200.h"]
 OUT = PKG / "libgazecut_b200.so"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -34,11 +36,20 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     stamp = OUT.with_suffix(".so.src")
     if not force and OUT.exists() and stamp.exists() and stamp.read_text() == digest:
         return OUT
-    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-           f"-I{ROOT / 'include'}", "-o", str(OUT), *map(str, SOURCES)]
+    objdir = PKG / "build"
+    objdir.mkdir(exist_ok=True)
+    common = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{ROOT / 'include'}"]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    subprocess.run(cmd, check=True)
+        common.insert(0, "-Xptxas=-v")
+    procs = []
+    for src in SOURCES:
+        obj = objdir / (src.stem + ".o")
+        procs.append((src, subprocess.Popen([nvcc(), *common, "-c", "-o", str(obj), str(src)])))
+    failed = [str(src) for src, pr in procs if pr.wait() != 0]
+    if failed:
+        raise RuntimeError(f"nvcc failed on {failed}")
+    subprocess.run([nvcc(), *ARCH, "-shared", "-o", str(OUT), *(str(objdir / (s_.stem + ".o")) for s_ in SOURCES),
+                    "-lcudart"], check=True)
     stamp.write_text(digest)
     return OUT
 

@@ -157,6 +157,7 @@ int gz_solve_volume_batch(const int32_t *vol, int32_t rows, int32_t cols, int32_
     if (!vol || !energies || !labels_out || n < 1 || rows < 1 || cols < 1 || m < 2) return GZ_ERR_ARG;
     for (int b = 0; b < n; ++b)
         if (energies[b].penalty < 0 || energies[b].inhibit < 0) return GZ_ERR_ARG;
+    if (!index_fits(rows, cols, m)) return GZ_ERR_OVERFLOW;
     const int P = rows * cols;
     const size_t one = ws_bytes(rows, cols, m);
     if (workspace_bytes < one) return GZ_ERR_WORKSPACE;
@@ -183,14 +184,13 @@ int gz_solve_volume_batch(const int32_t *vol, int32_t rows, int32_t cols, int32_
     if ((size_t)conc * one > workspace_bytes) conc = (int)(workspace_bytes / one);
     if (conc > n) conc = n;
     if (conc < 1) conc = 1;
-    static cudaStream_t streams[16];
-    static bool have = false;
-    if (!have) {
-        for (int k = 0; k < 16; ++k) CK(cudaStreamCreateWithFlags(&streams[k], cudaStreamNonBlocking));
-        have = true;
-    }
-    unsigned long long *pinned = nullptr;
-    CK(cudaHostAlloc((void **)&pinned, (size_t)n * gz::CTR_COUNT * 8, cudaHostAllocDefault));
+    DevicePool *pool = device_pool();
+    if (!pool) return GZ_ERR_CUDA;
+    std::lock_guard<std::mutex> lock(pool->mu);
+    if ((rc = pool->streams_ready())) return rc;
+    if ((rc = pool->pinned_ready((size_t)n * gz::CTR_COUNT))) return rc;
+    cudaStream_t *streams = pool->streams;
+    unsigned long long *pinned = pool->pinned;
     cudaEvent_t fork;
     CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
     CK(cudaEventRecord(fork, s));
@@ -223,7 +223,6 @@ int gz_solve_volume_batch(const int32_t *vol, int32_t rows, int32_t cols, int32_
         if (rc == GZ_OK) rc = r;
     }
     delete[] pend;
-    cudaFreeHost(pinned);
     if (rc) return rc;
     if (stats_out)
         for (int b = 0; b < n; ++b)

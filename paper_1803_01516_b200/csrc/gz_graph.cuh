@@ -77,6 +77,7 @@ struct Prob {
     int32_t *reach, *reach2, *labels;
     unsigned long long *ctr;  // counters, see CTR_*
     int sys;                  // row bands spanning GPUs: system-scope global atomics (gz_atomic_*)
+    int init_only;            // stop after the initialisation (graph export, gz_export_arcs)
 };
 
 // Global-memory atomics of the v4 solver that can land in another GPU's band

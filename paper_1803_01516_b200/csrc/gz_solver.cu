@@ -19,20 +19,13 @@
 // reachable in the residual graph from {source} U {nodes holding excess}; see
 // DESIGN.md section 3 for the argument and tests/test_gpu_parity.py for the
 // bit-exact checks against the oracle.
-#include <cooperative_groups.h>
-#include <cuda_runtime.h>
-
-#include <cstdint>
-#include <cstdio>
-#include <cstdlib>
-#include <cstring>
 #include <ctime>
 #include <unistd.h>
 
+#include <mutex>
 #include <vector>
 
-#include "gazecut_b200.h"
-#include "gz_graph.cuh"
+#include "gz_common.cuh"
 
 namespace cg = cooperative_groups;
 using namespace gz;
@@ -459,15 +452,6 @@ __device__ void phase_energy_col(const Prob &p, int c, long long &energy, int &v
     }
 }
 
-__device__ __forceinline__ void warp_add_u64(unsigned long long *dst, long long v, int sys = 0) {
-    unsigned long long x = (unsigned long long)v;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
-    if ((threadIdx.x & 31) == 0 && x) {
-        if (sys) atomicAdd_system(dst, x);
-        else atomicAdd(dst, x);
-    }
-}
 
 // ---------------------------------------------------------------------------
 // The whole solve in one cooperative launch: no host round trips.
@@ -605,9 +589,6 @@ __global__ void __launch_bounds__(256) gz_solve_kernel(Prob p) {
 
 }  // namespace
 
-#include "gz_bitsolve.cuh"
-#include "gz_chain.cuh"
-#include "gz_tilesolve.cuh"
 
 namespace {
 
@@ -784,6 +765,61 @@ size_t bit_bytes(int rows, int cols, int m) {
 // positions per site row of the v4 solver's node arrays (16, or 32 x segments; 0: m too large)
 int lanes_for(int m) { return m <= 16 ? 16 : (m <= 256 ? 32 * words_for(m) : 0); }
 
+#define CK(x)                                                                                  \
+    do {                                                                                       \
+        cudaError_t err__ = (x);                                                               \
+        if (err__ != cudaSuccess) {                                                            \
+            fprintf(stderr, "gazecut_b200: %s failed: %s\n", #x, cudaGetErrorString(err__));   \
+            return GZ_ERR_CUDA;                                                                \
+        }                                                                                      \
+    } while (0)
+
+// The kernels index node state with int32 (site * LPT + position for the v4
+// [site][LPT] planes, position * P + site for the v1 planar layout).  Problems
+// whose planes would exceed 2^31 - 1 elements are refused with GZ_ERR_OVERFLOW
+// instead of wrapping (C5, 3840 x 2160 x 256, is 2.12e9: inside, with ~1% to
+// spare; 4096 x 2160 x 256 is outside).
+bool index_fits(int rows, int cols, int m) {
+    const unsigned long long P = (unsigned long long)rows * (unsigned long long)cols;
+    const unsigned long long per = lanes_for(m) ? (unsigned long long)lanes_for(m) : (unsigned long long)m + 1;
+    return P * per <= 0x7fffffffull;
+}
+
+// Streams and the pinned counter buffer of the concurrent-solve entry points
+// (gz_solve_pairs, gz_solve_volume_batch), one set per device.  A call holds
+// its device's lock for its whole duration: calls on one device from several
+// host threads are serialised, calls on different devices run concurrently.
+struct DevicePool {
+    std::mutex mu;
+    cudaStream_t streams[16] = {};
+    bool have_streams = false;
+    unsigned long long *pinned = nullptr;
+    size_t pinned_n = 0;
+    int streams_ready() {
+        if (have_streams) return GZ_OK;
+        for (int k = 0; k < 16; ++k) CK(cudaStreamCreateWithFlags(&streams[k], cudaStreamNonBlocking));
+        have_streams = true;
+        return GZ_OK;
+    }
+    int pinned_ready(size_t n) {
+        if (pinned_n >= n) return GZ_OK;
+        if (pinned) cudaFreeHost(pinned);
+        pinned = nullptr;
+        pinned_n = 0;
+        CK(cudaHostAlloc((void **)&pinned, n * 8, cudaHostAllocDefault));
+        pinned_n = n;
+        return GZ_OK;
+    }
+};
+constexpr int MAX_DEVICES = 64;
+
+DevicePool *device_pool() {
+    static DevicePool pools[MAX_DEVICES];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= MAX_DEVICES) return nullptr;
+    return &pools[dev];
+}
+
 size_t ws_bytes(int rows, int cols, int m) {
     const int mp = m > lanes_for(m) ? m : lanes_for(m);
     const size_t P = (size_t)rows * cols, plane = align_up((size_t)mp * P * 4), col = align_up(P * 4);
@@ -817,14 +853,6 @@ Workspace carve(void *ws, int rows, int cols, int m) {
     return w;
 }
 
-#define CK(x)                                                                                  \
-    do {                                                                                       \
-        cudaError_t err__ = (x);                                                               \
-        if (err__ != cudaSuccess) {                                                            \
-            fprintf(stderr, "gazecut_b200: %s failed: %s\n", #x, cudaGetErrorString(err__));   \
-            return GZ_ERR_CUDA;                                                                \
-        }                                                                                      \
-    } while (0)
 
 int coop_grid(const void *kernel, int threads, int *grid_out, size_t dyn_smem = 0) {
     int dev = 0, sms = 0, occ = 0;
@@ -836,15 +864,12 @@ int coop_grid(const void *kernel, int threads, int *grid_out, size_t dyn_smem = 
     return GZ_OK;
 }
 
-// 1: v1 column relaxation (m > 256), 2: bit-parallel thread-per-chain
-// (deterministic relabel; the capped level-2 schedule), 4: tile-owned
-// warp-per-chain-segment solver with temporally blocked BFS (m <= 128, exact /
-// uncapped; the default).
+// 1: v1 column relaxation (m > 256, or forced with GZ_SCHED_V1 for
+// comparison), 4: tile-owned warp-per-chain-segment solver with temporally
+// blocked BFS (m <= 256; exact and capped level-2; the default).
 int choose_solver(int m, const gz_sched *sc) {
     const int flags = sc ? sc->flags : 0;
     if ((flags & GZ_SCHED_V1) || words_for(m) == 0) return 1;
-    if ((flags & GZ_SCHED_V2) || lanes_for(m) == 0) return 2;
-    if ((flags & GZ_SCHED_CAPPED) && getenv("GZ_CAPPED_V2")) return 2;
     return 4;
 }
 
@@ -926,6 +951,7 @@ struct Pending {
     int hard = 0, hcap = 0;
     volatile unsigned *progress = nullptr;
     int grid = 0;
+    int bfs_h = 0;   // BFS levels per blocked round (the capped schedule depends on it)
     unsigned long long *tbuf = nullptr;
 };
 
@@ -946,6 +972,7 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
     p.max_sweeps = sc ? sc->max_sweeps : 0;
     p.no_wave = sc ? (sc->flags & GZ_SCHED_NO_WAVE) : 0;
     p.capped = sc ? ((sc->flags & GZ_SCHED_CAPPED) != 0) : 0;
+    p.init_only = sc ? ((sc->flags & GZ_SCHED_INIT_ONLY) != 0) : 0;
     {
         const char *wd = getenv("GZ_WATCHDOG_MS");
         // default: 20 s plus 1 s per 2 M graph nodes (C3, 261 M nodes: ~150 s)
@@ -972,7 +999,6 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
     CK(cudaEventRecord(pd->e0, s));
     const bool win = lo != nullptr;
     const int NW = words_for(m);
-    const bool det = p.capped != 0;
     const int which = choose_solver(m, sc);
     const bool v1 = which == 1;
     // Exact v4 solves stop a relabel early once it is max(24, m) levels deep and has
@@ -1014,8 +1040,6 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
     }
     if (!v1 && p.bfs_cap < 0) p.bfs_cap = 0;            // exhaustive BFS every sweep
     const void *kern = nullptr;
-#define GZ_PICK(W_, NW_, D_) if (win == W_ && NW == NW_ && det == D_) kern = (const void *)gz2::gz_bitsolve_kernel<W_, NW_, D_>;
-#define GZ_PICK_NW(NW_) GZ_PICK(false, NW_, false) GZ_PICK(false, NW_, true) GZ_PICK(true, NW_, false) GZ_PICK(true, NW_, true)
     const int LPn = lanes_for(m);
     // two CTAs per SM (64 registers, smaller BFS regions) for the m <= 16 instance
     // (spills cost ~12% on a lone solve; with concurrent pair solves the doubled
@@ -1026,23 +1050,15 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
         occ4 = oc ? (atoi(oc) == 2 ? 2 : 1) : (conc >= 2 ? 2 : 1);
     }
     if (which == 4) {
-#define GZ_PICK4(LP_, R_, O_) if (LPn == LP_ * R_ && occ4 == O_) kern = win ? (const void *)gz4::gz_tilesolve_kernel<LP_, R_, true, O_> : (const void *)gz4::gz_tilesolve_kernel<LP_, R_, false, O_>;
-        GZ_PICK4(16, 1, 1) GZ_PICK4(16, 1, 2) GZ_PICK4(32, 1, 1) GZ_PICK4(32, 2, 1) GZ_PICK4(32, 4, 1)
-        GZ_PICK4(32, 8, 1)
-#undef GZ_PICK4
+        kern = LPn == 16 ? gz4::kernel_for(16, 1, win, occ4, 0) : gz4::kernel_for(32, LPn / 32, win, 1, 0);
         // windowed solves whose windows are at most 15 positions wide (the level-1/2
         // fine solves): window-relative 16-lane groups over the absolute rows
-        if (win && max_width >= 0 && max_width <= 15 && (LPn == 32 || LPn == 64) && !getenv("GZ_NO_REL")) {
-            kern = LPn == 32 ? (const void *)gz4::gz_tilesolve_kernel<16, 1, true, 1, 1>
-                             : (const void *)gz4::gz_tilesolve_kernel<16, 1, true, 1, 2>;
-        }
-    } else if (which == 2) {
-        GZ_PICK_NW(1) GZ_PICK_NW(2) GZ_PICK_NW(4) GZ_PICK_NW(8)
+        if (win && max_width >= 0 && max_width <= 15 && (LPn == 32 || LPn == 64) && !getenv("GZ_NO_REL"))
+            kern = gz4::kernel_for(16, 1, true, 1, LPn / 32);
     } else {
         kern = win ? (const void *)gz_solve_kernel<true> : (const void *)gz_solve_kernel<false>;
     }
-#undef GZ_PICK_NW
-#undef GZ_PICK
+    if (!kern) return GZ_ERR_ARG;
     if (!v1) CK(cudaMemsetAsync(w.bits_base, 0, w.bits_bytes, s));
     const int threads = which == 4 ? gz4::BLOCK : 256;
     const size_t dyn_smem = which == 4 ? gz4::smem_bytes(occ4) : 0;
@@ -1069,7 +1085,6 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
     gz2::Bits2 bb = w.bits;
     gz3::Arr3 a3{w.vol, w.cu, w.ph, w.pv, w.dar, w.dbr, w.dad, w.dbd, w.e, w.ein, w.h2, w.h, w.IN0, w.IN1};
     void *args1[] = {&p};
-    void *args2[] = {&p, &bb};
     void *args4[] = {&p, &bb, &a3, &geo, &bar};
     if (which == 4 && bp) {
         // row bands: one cooperative launch per band, forked from and joined to s
@@ -1101,12 +1116,13 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
         geo = tile_geo(rows, cols, grid, words_for(m), occ4);
         CK(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(threads), args4, dyn_smem, s));
     } else {
-        CK(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(256), which == 1 ? args1 : args2, 0, s));
+        CK(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(256), args1, 0, s));
     }
     CK(cudaEventRecord(pd->e1, s));
     pd->progress = p.progress;
     pd->tbuf = p.tbuf;
     pd->grid = grid;
+    pd->bfs_h = which == 4 ? (bp ? bp->geo.H : geo.H) : 1;
     CK(cudaMemcpyAsync(h_ctr, w.ctr, gz::CTR_COUNT * 8, cudaMemcpyDeviceToHost, s));
     if (labels_out && labels_out != w.labels)
         CK(cudaMemcpyAsync(labels_out, w.labels, (size_t)p.P * 4, cudaMemcpyDeviceToDevice, s));
@@ -1145,10 +1161,20 @@ int solve_finish(Pending &pd, gz_stats *st) {
         st->converged = (int32_t)h_ctr[CTR_CONVERGED];
         st->energy = st->converged ? st->flow + st->const_offset : st->labeling_energy;
         st->sweeps = (int32_t)h_ctr[CTR_SWEEPS];
-        st->stranded_excess_nodes = (int32_t)h_ctr[CTR_STRANDED];
+        // maxflow.py:466-470 counts nodes still holding excess when the solve stops.
+        // The reference drains excess back to the source (phase 2), so a converged
+        // solve leaves none: every node with excess in a preflow has a residual
+        // path back to the source, so it stays active until drained.  This solver
+        // stops after phase 1 and its leftover excess is
+        // exactly what phase 2 would return; the converged count is therefore 0,
+        // like the reference's.  Capped solves report the nodes holding excess
+        // at the stop (the level-2 state the labeling is read from).
+        st->excess_nodes = (int32_t)h_ctr[CTR_STRANDED];
+        st->stranded_excess_nodes = st->converged ? 0 : st->excess_nodes;
         st->bfs_passes = (int32_t)h_ctr[CTR_BFS_PASSES];
         st->reach_passes = (int32_t)h_ctr[CTR_REACH_PASSES];
         st->pulses = (int32_t)h_ctr[CTR_PULSES];
+        st->bfs_h = pd.bfs_h;
         st->ms_total = ms;
         for (int q = 0; q < 6; ++q) st->ms_phase[q] = (float)(h_ctr[CTR_T0 + q] * 1e-6);
     }
@@ -1180,6 +1206,17 @@ int solve_planar(const Workspace &w, int rows, int cols, int m, const gz_energy 
     return solve_finish(pd, st);
 }
 
+}  // namespace
+
+const void *gz4::kernel_for(int LP, int R, bool win, int occ, int rw) {
+    if (LP == 16) return kernels_lp16(win, occ, rw);
+    if (LP == 32 && R <= 2) return kernels_lp32(R, win);
+    if (LP == 32) return kernels_lp32w(R, win);
+    return nullptr;
+}
+
+namespace {
+
 int check_sm100() {
     int dev = 0, major = 0;
     CK(cudaGetDevice(&dev));
@@ -1194,7 +1231,7 @@ int check_sm100() {
 extern "C" {
 
 size_t gz_workspace_bytes(int32_t rows, int32_t cols, int32_t m) {
-    if (rows < 1 || cols < 1 || m < 1) return 0;
+    if (rows < 1 || cols < 1 || m < 1 || !index_fits(rows, cols, m)) return 0;
     return ws_bytes(rows, cols, m);
 }
 
@@ -1202,6 +1239,10 @@ int gz_sad_volume(const uint8_t *left, const uint8_t *right, int32_t img_h, int3
                   const gz_cuboid *cb, int32_t *vol_out, void *stream) {
     if (!cb || !left || !right || !vol_out || channels < 1) return GZ_ERR_ARG;
     if (cb->y_min < 0 || cb->y_min + cb->y_extent > img_h || cb->g_extent < 1 || cb->m < 1) return GZ_ERR_ARG;
+    // columns are clamped to [0, width-1] and rows are img_w pixels apart: a
+    // cuboid wider than the image would read past the rows (the reference raises
+    // IndexError there, geometry.py:325-335)
+    if (cb->width < 1 || cb->width > img_w) return GZ_ERR_ARG;
     const int P = cb->y_extent * cb->g_extent;
     k_sad<0><<<(P + 127) / 128, 128, 0, (cudaStream_t)stream>>>(left, right, img_w, channels, *cb, vol_out);
     CK(cudaGetLastError());
@@ -1213,6 +1254,7 @@ int gz_solve_volume(const int32_t *vol, int32_t rows, int32_t cols, int32_t m, c
                     gz_stats *stats_out, void *workspace, size_t workspace_bytes, void *stream) {
     if (!vol || !energy || rows < 1 || cols < 1 || m < 1 || (!lo) != (!hi)) return GZ_ERR_ARG;
     if (energy->penalty < 0 || energy->inhibit < 0) return GZ_ERR_ARG;
+    if (!index_fits(rows, cols, m)) return GZ_ERR_OVERFLOW;
     if (workspace_bytes < ws_bytes(rows, cols, m)) return GZ_ERR_WORKSPACE;
     int rc = check_sm100();
     if (rc) return rc;
@@ -1272,8 +1314,10 @@ int gz_solve_pairs(const uint8_t *left, const uint8_t *right, int32_t batch, int
                    int32_t *labels_out, gz_stats *stats_out, void *workspace, size_t workspace_bytes,
                    void *stream) {
     if (!cb || !energy || batch < 1 || channels < 1 || cb->m < 2) return GZ_ERR_ARG;
-    if (cb->y_min < 0 || cb->y_min + cb->y_extent > img_h) return GZ_ERR_ARG;
+    if (cb->y_min < 0 || cb->y_min + cb->y_extent > img_h || cb->width > img_w || cb->width < 1) return GZ_ERR_ARG;
+    if (cb->g_extent < 1 || cb->y_extent < 1) return GZ_ERR_ARG;
     const int rows = cb->y_extent, cols = cb->g_extent, m = cb->m, P = rows * cols;
+    if (!index_fits(rows, cols, m)) return GZ_ERR_OVERFLOW;
     const size_t one = ws_bytes(rows, cols, m);
     if (workspace_bytes < one) return GZ_ERR_WORKSPACE;
     int rc = check_sm100();
@@ -1292,19 +1336,13 @@ int gz_solve_pairs(const uint8_t *left, const uint8_t *right, int32_t batch, int
     if ((size_t)conc * one > workspace_bytes) conc = (int)(workspace_bytes / one);
     if (conc > batch) conc = batch;
     if (which != 4 || conc < 1) conc = 1;
-    static cudaStream_t streams[16];
-    static bool have_streams = false;
-    static unsigned long long *pinned = nullptr;
-    static size_t pinned_n = 0;
-    if (conc > 1 && !have_streams) {
-        for (int k = 0; k < 16; ++k) CK(cudaStreamCreateWithFlags(&streams[k], cudaStreamNonBlocking));
-        have_streams = true;
-    }
-    if (pinned_n < (size_t)batch * gz::CTR_COUNT) {
-        if (pinned) cudaFreeHost(pinned);
-        pinned_n = (size_t)batch * gz::CTR_COUNT;
-        CK(cudaHostAlloc((void **)&pinned, pinned_n * 8, cudaHostAllocDefault));
-    }
+    DevicePool *pool = device_pool();
+    if (!pool) return GZ_ERR_CUDA;
+    std::lock_guard<std::mutex> lock(pool->mu);
+    if (conc > 1 && (rc = pool->streams_ready())) return rc;
+    if ((rc = pool->pinned_ready((size_t)batch * gz::CTR_COUNT))) return rc;
+    cudaStream_t *streams = pool->streams;
+    unsigned long long *pinned = pool->pinned;
     cudaEvent_t fork = nullptr;
     if (conc > 1) {
         CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
@@ -1439,7 +1477,10 @@ int gz_coarsen(const int32_t *vol, int32_t rows, int32_t cols, int32_t m, int32_
 
 int gz_thin_skin(const int32_t *coarse_labels, int32_t crows, int32_t ccols, int32_t rows, int32_t cols, int32_t m,
                  int32_t block, int32_t radius, int32_t *lo_out, int32_t *hi_out, void *stream) {
-    if (!coarse_labels || !lo_out || !hi_out || block < 1 || radius < 0) return GZ_ERR_ARG;
+    if (!coarse_labels || !lo_out || !hi_out || block < 1 || radius < 0 || rows < 1 || cols < 1 || m < 1)
+        return GZ_ERR_ARG;
+    // the coarse grid must cover the fine one (k_thin_skin reads coarse[(y/b, g/b)])
+    if ((long long)crows * block < rows || (long long)ccols * block < cols) return GZ_ERR_ARG;
     const int P = rows * cols;
     k_thin_skin<<<(P + 255) / 256, 256, 0, (cudaStream_t)stream>>>(coarse_labels, crows, ccols, rows, cols, m, block,
                                                                   radius, lo_out, hi_out);
@@ -1468,3 +1509,4 @@ const char *gz_build_info(void) { return "gazecut_b200 v4 sm_100a tile-owned per
 
 #include "gz_bands.cuh"
 #include "gz_eval.cuh"
+#include "gz_csr.cuh"

@@ -404,6 +404,10 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
     for (int i = ttid; i < bwords; i += tstride) b.IN[band_word(i)] = 1u;   // every site starts dirty
     TEAM_SYNC();
     TICK(0);
+    if (p.init_only) {   // graph export: the state planes now hold the capacities
+        warp_add_u64(&p.ctr[CTR_OFFSET], offset, p.sys);
+        return;
+    }
     int sweeps = 0, levels_total = 0, pulses = 0, parity = 0;
     int converged = 1;
     bool err = false;

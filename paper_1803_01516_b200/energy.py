@@ -86,6 +86,10 @@ def sad_volume_device(left, right, cuboid: CuboidSpec, width: int | None = None)
     h, w, ch = _images(left, right)
     width = w if width is None else width
     cuboid.check_consistent(width, h)
+    if width > w:
+        # the reference gathers columns clipped to [0, width-1] from the images and
+        # fails with IndexError past their edge (geometry.py:325-335)
+        raise IndexError(f"cuboid width {width} exceeds the image width {w}")
     dl, dr = _dev.as_device_u8(left), _dev.as_device_u8(right)
     out = torch.empty((cuboid.y_extent, cuboid.g_extent, cuboid.num_labels), dtype=torch.int32, device=dl.device)
     cs = cuboid_struct(cuboid, width)

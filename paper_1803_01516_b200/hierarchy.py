@@ -59,6 +59,9 @@ def thin_skin(coarse_labeling, fine_shape, block: int, radius: int = DEFAULT_SKI
     """hierarchy.py:60-73: windows [b(D-r), b(D+r+1)-1] clamped to [0, m-1]."""
     lab = _dev.as_device_i32(coarse_labeling, "coarse_labeling")
     rows, cols, _ = fine_shape
+    if lab.dim() != 2 or int(lab.shape[0]) * block < rows or int(lab.shape[1]) * block < cols:
+        raise ValueError(f"coarse labeling {tuple(lab.shape)} x block {block} does not cover the fine grid "
+                         f"{(rows, cols)}")
     lo, hi = thin_skin_device(lab, fine_shape, block, radius)
     return lo.view(rows, cols).cpu().numpy(), hi.view(rows, cols).cpu().numpy()
 

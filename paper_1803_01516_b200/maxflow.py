@@ -89,6 +89,8 @@ def maxflow_push_relabel(net: FlowNetwork, rounds_per_sweep: int = 12, max_sweep
         "relabels": int(st.relabels),
         "presaturated": int(st.presaturated),
         "stranded_excess_nodes": int(st.stranded_excess_nodes),
+        "excess_nodes": int(st.excess_nodes),
+        "bfs_h": int(st.bfs_h),
         "device": "sm_100a",
         "device_ms": float(st.ms_total),
         "pulses": int(st.pulses),

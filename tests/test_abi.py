@@ -63,3 +63,54 @@ def test_argument_errors_without_a_gpu():
     one = _lib.Cuboid(384, 288, -186, 372, 0, 288, 175, 1)
     assert L.gz_solve_pairs(p, p, 1, 288, 384, 3, C.byref(one), C.byref(en), C.byref(sc), p, C.byref(st), p,
                             1 << 30, None) == _lib.GZ_ERR_ARG
+
+
+def test_int32_index_boundary():
+    """Node indices are int32 on the device (site * LPT + position).  C5
+    (2160 x 3827 sites x 256 labels, 2.12e9 node slots) fits; 4096-wide 4K at
+    256 labels (2.26e9) is refused with GZ_ERR_OVERFLOW instead of wrapping."""
+    import ctypes as C
+    L = _lib.lib()
+    assert L.gz_workspace_bytes(2160, 3827, 256) > 100 * 2**30
+    assert L.gz_workspace_bytes(2160, 4096, 256) == 0
+    assert L.gz_workspace_bytes(65536, 32768, 2) == 0          # 2^31 sites x 16 lanes
+    en = _lib.Energy(14, 1023, 0)
+    sc = _lib.Sched(12, 0, 0, 0)
+    st = _lib.Stats()
+    p = C.c_void_p(16)
+    assert L.gz_solve_volume(p, 2160, 4096, 256, C.byref(en), C.byref(sc), None, None, p, C.byref(st), p,
+                             1 << 62, None) == _lib.GZ_ERR_OVERFLOW
+    assert L.gz_solve_volume_batch(p, 2160, 4096, 256, C.byref(en), 1, C.byref(sc), p, C.byref(st), p, 1 << 62,
+                                   None) == _lib.GZ_ERR_OVERFLOW
+    devs = (C.c_int32 * 1)(0)
+    assert L.gz_solve_volume_banded(p, 2160, 4096, 256, C.byref(en), C.byref(sc), None, None, 1, devs, p,
+                                    C.byref(st)) == _lib.GZ_ERR_OVERFLOW
+    cub = _lib.Cuboid(4610, 2160, -2304, 4096, 0, 2160, 2000, 256)
+    assert L.gz_solve_pairs(p, p, 1, 2160, 4610, 3, C.byref(cub), C.byref(en), C.byref(sc), p, C.byref(st), p,
+                            1 << 62, None) == _lib.GZ_ERR_OVERFLOW
+
+
+def test_cuboid_wider_than_image_is_rejected():
+    """k_sad clamps columns to width-1 but strides rows by the image width: a
+    cuboid wider than the image is an argument error (IndexError upstream)."""
+    import ctypes as C
+    L = _lib.lib()
+    cub = _lib.Cuboid(400, 288, -186, 372, 0, 288, 175, 16)
+    p = C.c_void_p(16)
+    assert L.gz_sad_volume(p, p, 288, 384, 3, C.byref(cub), p, None) == _lib.GZ_ERR_ARG
+    en = _lib.Energy(14, 1023, 0)
+    sc = _lib.Sched(12, 0, 0, 0)
+    st = _lib.Stats()
+    assert L.gz_solve_pairs(p, p, 1, 288, 384, 3, C.byref(cub), C.byref(en), C.byref(sc), p, C.byref(st), p,
+                            1 << 30, None) == _lib.GZ_ERR_ARG
+    # thin_skin: the coarse grid must cover the fine one
+    assert L.gz_thin_skin(p, 10, 10, 31, 20, 16, 3, 1, p, p, None) == _lib.GZ_ERR_ARG
+
+
+def test_stats_struct_matches_header():
+    """ctypes Stats mirrors gz_stats field for field (new fields append)."""
+    text = (ROOT / "include" / "gazecut_b200.h").read_text()
+    body = text[text.index("typedef struct {\n    int64_t flow"):]
+    body = body[: body.index("} gz_stats;")]
+    names = re.findall(r"\b([a-z_][a-z_0-9]*)(?:\[\d+\])?\s*[,;]", re.sub(r"/\*.*?\*/", "", body, flags=re.S))
+    assert names == [f[0] for f in _lib.Stats._fields_]

@@ -99,3 +99,36 @@ def test_band_worklists_forced(gz, monkeypatch, m):
     for nb in (1, 3):
         r = gz.solve_exact_bands(vol, p, devices=(0,) * nb)
         assert r.flow == one.flow and np.array_equal(r.labeling, one.labeling), (m, nb)
+
+
+@pytest.fixture
+def force_sys(monkeypatch):
+    """GZ_FORCE_SYS=1: the multi-device band path on one GPU -- system-scope
+    fences and atomics in the team barrier and on cross-band state, and one
+    physical VMM allocation per band."""
+    monkeypatch.setenv("GZ_FORCE_SYS", "1")
+
+
+@pytest.mark.parametrize("nbands", [2, 4])
+def test_c1_bands_forced_system_scope(gz, force_sys, nbands):
+    cub = gz.cuboid_from_disparity_range(384, 288, 10, 28, num_labels=16)
+    for seed in (0, 3):
+        sc = gz.make_scene(seed)
+        vol = gz.sad_volume(sc.left, sc.right, cub)
+        r = gz.solve_exact_bands(vol, gz.EnergyParams(14, 1023), devices=(0,) * nbands)
+        want = G["c1_exact"][seed]
+        assert r.flow == want["flow"] and r.energy == want["energy"], (seed, nbands)
+        assert sha(r.labeling) == want["labeling"], (seed, nbands)
+
+
+@pytest.mark.parametrize("m,nbands", [(40, 2), (100, 4)])
+def test_random_bands_forced_system_scope(gz, force_sys, m, nbands):
+    rng = np.random.default_rng(2000 + m)
+    rows, cols = 96, 80
+    vol = rng.integers(0, 200, size=(rows, cols, m)).astype(np.int64)
+    for hard in (False, True):
+        p = gz.EnergyParams(9, 40, hard)
+        one = gz.solve_exact(vol, p)
+        r = gz.solve_exact_bands(vol, p, devices=(0,) * nbands)
+        assert (r.flow, r.energy) == (one.flow, one.energy), (m, nbands, hard)
+        assert np.array_equal(r.labeling, one.labeling), (m, nbands, hard)

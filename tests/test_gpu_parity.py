@@ -155,3 +155,17 @@ def test_narrow_windows_match_oracle(gz, oracle, m):
         assert net.const_offset == onet.const_offset
         assert got.flow == flow and got.energy == energy, (m, k)
         assert np.array_equal(got.labeling, lab) and np.array_equal(got.source_side, side)
+
+
+@pytest.mark.parametrize("m,hard", [(300, False), (300, True), (400, False)])
+def test_v1_solver_beyond_256_labels(gz, oracle, m, hard):
+    """m > 256 runs the v1 planar column-relaxation solver (choose_solver in
+    gz_solver.cu); it must agree with the reference restatement bit for bit."""
+    rng = np.random.default_rng(m + hard)
+    vol = rng.integers(0, 60, size=(6, 7, m)).astype(np.int64)
+    p = gz.EnergyParams(3, 11, hard)
+    got = gz.solve_exact(vol, p)
+    want = oracle.solve_exact(vol, 3, 11, hard)
+    assert got.flow == want["flow"] and got.energy == want["energy"]
+    assert np.array_equal(got.labeling, want["labeling"])
+    assert got.stats["stranded_excess_nodes"] == 0

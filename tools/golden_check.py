@@ -1,4 +1,4 @@
-"""Run the golden random cases through the default (v4) and the v2 solver; print the first mismatches."""
+"""Run the golden random cases through the v1 (forced with GZ_SCHED_V1) and the default v4 solver; print the first mismatches."""
 import ctypes as C, json, sys
 from pathlib import Path
 ROOT = Path(__file__).resolve().parent.parent
@@ -31,12 +31,12 @@ for i, meta in enumerate(G["random_cases"]):
     hi = arr[f"hi{i}"] if meta["windowed"] else None
     net = gz.build_network(arr[f"vol{i}"], p, lo, hi)
     out = []
-    for fl in (_lib.GZ_SCHED_V2, 0):
+    for fl in (_lib.GZ_SCHED_V1, 0):
         rc, lab, st = run(net, fl)
         out.append((rc, st.flow, st.sweeps, st.pulses, st.bfs_passes, st.pushes, st.relabels, st.presaturated, st.reach_passes))
     if out[0][1] != out[1][1] or out[1][1] != meta["flow"]:
         bad += 1
-        print(i, arr[f"vol{i}"].shape, meta["windowed"], meta["hard"], "want", meta["flow"], "v2", out[0], "v4", out[1], flush=True)
+        print(i, arr[f"vol{i}"].shape, meta["windowed"], meta["hard"], "want", meta["flow"], "v1", out[0], "v4", out[1], flush=True)
         if bad > 8:
             break
 print("bad", bad)
