@@ -224,11 +224,15 @@ int gz_thin_skin(const int32_t *coarse_labels, int32_t crows, int32_t ccols, int
  * capacity; node ids as flownet.py numbers them, source = n-2, sink = n-1), or
  * all NULL to count only.  info (host int64[4]): [0] pairs, [1] the constant
  * offset folded by the export, [2] nodes, [3] the constant offset of the
- * device initialisation (the two must agree).  Exact pairs for m <= 256. */
+ * device initialisation (the two must agree).  m <= 256.
+ * residual = 1: no initialisation; the pairs carry the forward and reverse
+ * RESIDUALS of the state the last solve in `workspace` left (vol unused; the
+ * same windows): the preflow in the reference's arc order, for
+ * maxflow.py-style inspection of a solved grid network. */
 int gz_export_arcs(const int32_t *vol, int32_t rows, int32_t cols, int32_t m, const gz_energy *energy,
-                   const int32_t *lo, const int32_t *hi, int64_t *pair_u, int64_t *pair_v, int64_t *pair_cap,
-                   int64_t *pair_rcap, int64_t capacity, int64_t *info, void *workspace, size_t workspace_bytes,
-                   void *stream);
+                   const int32_t *lo, const int32_t *hi, int32_t residual, int64_t *pair_u, int64_t *pair_v,
+                   int64_t *pair_cap, int64_t *pair_rcap, int64_t capacity, int64_t *info, void *workspace,
+                   size_t workspace_bytes, void *stream);
 
 /* One state plane of the last v4 solve run in `workspace` (m <= 256), as
  * int32 (rows*cols, m-1), position t at column t-1: the certificate input
@@ -261,15 +265,23 @@ size_t gz_csr_workspace_bytes(int64_t n_nodes);
  * (flownet.py:41-89 FlowNetwork arrays; flownet.py:325-353 network_from_arcs):
  * source saturation, global relabeling (sink distance, n + source distance,
  * 2n parked: maxflow.py:138-170) and rounds_per_sweep synchronous pulses per
- * sweep until no active node remains (or max_sweeps >= 0 sweeps ran).  Both
+ * sweep until no active node remains (or max_sweeps >= 0 sweeps ran).  The
+ * run starts from the flow already in `resid` (excess = -(net outflow of
+ * cap - resid): a presaturated or partially solved network).  Both
  * phases run, so `resid` (device int64, updated in place) ends as a maximum
  * flow with no excess left, like the reference's.  side_out (device uint8[n],
  * or NULL): maxflow.py:267-284 source side.  excess_out (device int64[n] or
  * NULL).  Device pointers except stats_out (host). */
 int gz_maxflow_csr(int64_t n_nodes, int64_t source, int64_t sink, const int64_t *first_out, const int32_t *head,
-                   const int32_t *rev, int64_t *resid, int32_t rounds_per_sweep, int32_t max_sweeps,
+                   const int32_t *rev, const int64_t *cap, int64_t *resid, int32_t rounds_per_sweep, int32_t max_sweeps,
                    uint8_t *side_out, int64_t *excess_out, gz_csr_stats *stats_out, void *workspace,
                    size_t workspace_bytes, void *stream);
+
+/* maxflow.py:267-284 _bfs_source_side / maxflow.py:355-359 source_side on
+ * CSR arrays: side_out (device uint8[n]) = reachable from the source over
+ * resid > 0.  Synchronous. */
+int gz_source_side_csr(int64_t n_nodes, int64_t source, const int64_t *first_out, const int32_t *head,
+                       const int64_t *resid, uint8_t *side_out, void *stream);
 
 /* maxflow.py:287-304 _chain_presaturate on CSR arrays (device; sent_out is a
  * device int64). */

@@ -8,14 +8,18 @@ hand-written sm_100a CUDA kernels in ``libgazecut_b200.so`` behind a C ABI
 (include/gazecut_b200.h).  There is no CPU fallback.
 
 Accuracy accounting (ground truth -> depth numbers, error counts, penalty
-sweeps) also runs on the device.  Out of scope: image file I/O,
-CSV reports, the CLI and generic CSR networks.
+sweeps) also runs on the device, and so do explicit networks: the reference's
+CSR arrays exported from the device graph, generic ``network_from_arcs``
+networks and the CSR solver behind ``maxflow_reference``.
 """
 
 from .energy import UNCUTTABLE, EnergyParams, pairwise_term, sad_volume, sad_volume_device, total_energy
 from .flownet import (
     FlowNetwork,
     build_network,
+    dump_network,
+    node_blocks,
+    pairs_to_csr,
     expected_arc_count,
     expected_node_count,
     full_windows,
@@ -50,6 +54,8 @@ from .hierarchy import coarsen, solve_level1, solve_level2, thin_skin
 from .maxflow import (
     CutResult,
     InternalConsistencyError,
+    chain_presaturate,
+    conservation_violations,
     extract_labeling,
     maxflow_push_relabel,
     maxflow_reference,
@@ -88,5 +94,6 @@ __all__ = [
     "maxflow_push_relabel", "maxflow_reference", "network_from_arcs", "pairwise_term",
     "pixels_from_gaze_depth", "sad_volume", "sad_volume_device", "solve_exact", "solve_level1",
     "solve_level2", "solve_exact_bands", "solve_pairs", "source_side", "thin_skin", "total_energy", "whs_from_disparity",
+    "chain_presaturate", "conservation_violations", "dump_network", "node_blocks", "pairs_to_csr",
     "__version__",
 ]

@@ -62,12 +62,32 @@ def as_device_u8(a) -> torch.Tensor:
 
 
 _WS: dict = {}
+_WS_GEN = [0]
 
 
 def workspace(nbytes: int) -> torch.Tensor:
-    """A cached device workspace of at least ``nbytes`` (per device)."""
+    """A cached device workspace of at least ``nbytes`` (per device).  Every
+    call starts a new generation: state a solve left in the workspace is valid
+    only while the generation it was solved in is current."""
     dev = require_gpu()
     buf = _WS.get(dev.index)
     if buf is None or buf.numel() < nbytes:
         _WS[dev.index] = buf = torch.empty(int(nbytes), dtype=torch.uint8, device=dev)
+    _WS_GEN[0] += 1
+    return buf
+
+
+def workspace_generation() -> int:
+    return _WS_GEN[0]
+
+
+_CSR_WS: dict = {}
+
+
+def csr_workspace(nbytes: int) -> torch.Tensor:
+    """Workspace of the CSR kernels (separate from the grid solver's)."""
+    dev = require_gpu()
+    buf = _CSR_WS.get(dev.index)
+    if buf is None or buf.numel() < nbytes:
+        _CSR_WS[dev.index] = buf = torch.empty(int(nbytes), dtype=torch.uint8, device=dev)
     return buf

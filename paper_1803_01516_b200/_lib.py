@@ -27,6 +27,10 @@ GZ_SCHED_CAPPED = 2
 GZ_SCHED_V1 = 4
 GZ_SCHED_V2 = 8   # retired (maps to the default v4 solver)
 GZ_SCHED_V3 = 16  # retired (maps to the default v4 solver)
+GZ_SCHED_INIT_ONLY = 32
+# gz_export_state planes (include/gazecut_b200.h enum gz_plane)
+GZ_PLANE_CHAIN, GZ_PLANE_SAME_RIGHT, GZ_PLANE_SAME_DOWN, GZ_PLANE_DIAG_RIGHT, GZ_PLANE_DIAG_LEFT, \
+    GZ_PLANE_DIAG_DOWN, GZ_PLANE_DIAG_UP, GZ_PLANE_EXCESS, GZ_PLANE_HEIGHT = range(9)
 
 
 class Cuboid(C.Structure):
@@ -57,6 +61,11 @@ class Stats(C.Structure):
                 ("sweeps", "converged", "stranded_excess_nodes", "bfs_passes", "reach_passes",
                  "pulses", "bfs_h", "excess_nodes")] + \
                [("ms_total", C.c_float), ("ms_phase", C.c_float * 6)]
+
+
+class CsrStats(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("flow", "pushes", "relabels", "stranded_excess_nodes")] + \
+               [(n, C.c_int32) for n in ("sweeps", "converged", "pulses")] + [("ms_total", C.c_float)]
 
 
 class GazecutError(RuntimeError):
@@ -112,6 +121,23 @@ def lib():
         L.gz_coarsen.argtypes = [_vp, _i32, _i32, _i32, _i32, _vp, _vp]
         L.gz_thin_skin.restype = C.c_int
         L.gz_thin_skin.argtypes = [_vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp]
+        _i64 = C.c_int64
+        L.gz_export_arcs.restype = C.c_int
+        L.gz_export_arcs.argtypes = [_vp, _i32, _i32, _i32, C.POINTER(Energy), _vp, _vp, _i32, _vp, _vp, _vp, _vp,
+                                     _i64, _vp, _vp, C.c_size_t, _vp]
+        L.gz_export_state.restype = C.c_int
+        L.gz_export_state.argtypes = [_vp, _i32, _i32, _i32, _i32, _vp, _vp]
+        L.gz_csr_workspace_bytes.restype = C.c_size_t
+        L.gz_csr_workspace_bytes.argtypes = [_i64]
+        L.gz_maxflow_csr.restype = C.c_int
+        L.gz_maxflow_csr.argtypes = [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp,
+                                     C.POINTER(CsrStats), _vp, C.c_size_t, _vp]
+        L.gz_source_side_csr.restype = C.c_int
+        L.gz_source_side_csr.argtypes = [_i64, _i64, _vp, _vp, _vp, _vp, _vp]
+        L.gz_chain_presaturate_csr.restype = C.c_int
+        L.gz_chain_presaturate_csr.argtypes = [_vp, _vp, _vp, _vp, _i64, _vp, _vp]
+        L.gz_conservation_violations_csr.restype = C.c_int
+        L.gz_conservation_violations_csr.argtypes = [_vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp]
         L.gz_status_string.restype = C.c_char_p
         L.gz_status_string.argtypes = [C.c_int]
         L.gz_build_info.restype = C.c_char_p
@@ -136,5 +162,6 @@ EXPORTED = (
     "gz_workspace_bytes", "gz_sad_volume", "gz_solve_volume", "gz_solve_pairs",
     "gz_solve_pairs_host", "gz_solve_volume_banded", "gz_ground_truth_to_depth",
     "gz_error_count", "gz_render_disparity", "gz_solve_volume_batch", "gz_total_energy", "gz_coarsen", "gz_thin_skin",
-    "gz_status_string", "gz_build_info",
+    "gz_status_string", "gz_build_info", "gz_export_arcs", "gz_export_state", "gz_csr_workspace_bytes",
+    "gz_maxflow_csr", "gz_source_side_csr", "gz_chain_presaturate_csr", "gz_conservation_violations_csr",
 )

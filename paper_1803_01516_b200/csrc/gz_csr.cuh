@@ -49,7 +49,11 @@ __device__ __forceinline__ long long x_node(const ExportArgs &x, int s, int lo, 
 // One thread per site, the emission order of flownet.py:115-180: chain arcs by
 // label, then per forward neighbour (right, down) and level t: the same-level
 // pair, then both inhibit diagonals.
-template <bool FILL>
+// MODE 0: capacities of the initialised graph (cap, rcap); MODE 1: residuals of
+// the state a solve left (resid forward, resid reverse).  Arcs out of the
+// source are saturated at initialisation and a solve never pushes into source
+// positions (gz_chain.cuh), so in MODE 1 they read (0, cap + rcap).
+template <bool FILL, int MODE = 0>
 __global__ void k_export_arcs(ExportArgs x) {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     const int P = x.rows * x.cols;
@@ -61,6 +65,7 @@ __global__ void k_export_arcs(ExportArgs x) {
     unsigned long long off = 0;
     const unsigned long long UNC = (unsigned long long)gz::UNCUTTABLE;
     auto emit = [&](long long a, long long b, long long c, long long rc) {
+        if (MODE == 1 && a == x.src) { rc += c; c = 0; }
         if (FILL) {
             x.pu[k] = a; x.pv_[k] = b; x.pc[k] = c; x.prc[k] = rc;
             ++k;
@@ -74,7 +79,8 @@ __global__ void k_export_arcs(ExportArgs x) {
         // position 0 has no residual slot and is read from the data-term plane
         const long long cap = lab == 0 ? x.vol[row] : x.cu[row + lab - 1];
         if (a == x.src && b == x.snk) off += (unsigned long long)cap;
-        else emit(a, b, cap, (long long)UNC);
+        else if (MODE == 0 || a == x.src) emit(a, b, cap, (long long)UNC);
+        else emit(a, b, cap, (long long)UNC + (x.vol[row + lab] - cap));   // cu = residual; flow = vol - cu
     }
     for (int nb = 0; nb < 2; ++nb) {
         const int yn = nb == 0 ? y : y + 1, gn = nb == 0 ? g + 1 : g;
@@ -151,6 +157,7 @@ struct CsrArgs {
     long long n, source, sink;
     const long long *first_out;
     const int32_t *head, *rev;
+    const long long *cap;
     long long *resid, *excess, *ein;
     int *h, *pushed;
     unsigned char *side;
@@ -179,6 +186,14 @@ __global__ void __launch_bounds__(256) k_csr_solve(CsrArgs a) {
     const long long n = a.n, hmax = 2 * n;
     int rot = 0;
     long long pushes = 0, relabels = 0;
+    // excess of the flow already in the network (a presaturated chain, or the
+    // preflow a grid solve left behind): minus the net outflow cap - resid
+    for (long long v = tid; v < n; v += stride) {
+        long long out = 0;
+        for (long long q = a.first_out[v]; q < a.first_out[v + 1]; ++q) out += a.cap[q] - a.resid[q];
+        a.excess[v] = -out;
+    }
+    grid.sync();
     // maxflow.py:173-180 _saturate_source
     for (long long q = a.first_out[a.source] + tid; q < a.first_out[a.source + 1]; q += stride) {
         const long long f = a.resid[q];
@@ -297,6 +312,30 @@ __global__ void __launch_bounds__(256) k_csr_solve(CsrArgs a) {
     }
 }
 
+// maxflow.py:267-284 _bfs_source_side on its own (no solve): level-synchronous
+__global__ void __launch_bounds__(256) k_csr_side(long long n, long long source, const long long *first_out,
+                                                  const int32_t *head, const long long *resid, unsigned char *side,
+                                                  unsigned long long *slots) {
+    cg::grid_group grid = cg::this_grid();
+    const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    int rot = 0;
+    for (long long v = tid; v < n; v += stride) side[v] = v == source ? 1 : 0;
+    grid.sync();
+    for (;;) {
+        bool ch = false;
+        for (long long u = tid; u < n; u += stride) {
+            if (!side[u]) continue;
+            for (long long q = first_out[u]; q < first_out[u + 1]; ++q)
+                if (resid[q] > 0 && !side[head[q]]) {
+                    side[head[q]] = 1;
+                    ch = true;
+                }
+        }
+        if (!grid_any(grid, slots, rot, ch)) break;
+    }
+}
+
 // maxflow.py:287-304: per chain, push the chain's smallest residual through it
 __global__ void k_chain_presaturate(const int32_t *rev, long long *resid, const int32_t *chain_arcs,
                                     const long long *chain_base, long long nsites, unsigned long long *total) {
@@ -338,10 +377,10 @@ __global__ void k_conservation(const long long *first_out, const long long *cap,
 extern "C" {
 
 int gz_export_arcs(const int32_t *vol, int32_t rows, int32_t cols, int32_t m, const gz_energy *energy,
-                   const int32_t *lo, const int32_t *hi, int64_t *pair_u, int64_t *pair_v, int64_t *pair_cap,
-                   int64_t *pair_rcap, int64_t capacity, int64_t *info, void *workspace, size_t workspace_bytes,
-                   void *stream) {
-    if (!vol || !energy || !info || rows < 1 || cols < 1 || m < 1 || (!lo) != (!hi)) return GZ_ERR_ARG;
+                   const int32_t *lo, const int32_t *hi, int32_t residual, int64_t *pair_u, int64_t *pair_v,
+                   int64_t *pair_cap, int64_t *pair_rcap, int64_t capacity, int64_t *info, void *workspace,
+                   size_t workspace_bytes, void *stream) {
+    if ((!vol && !residual) || !energy || !info || rows < 1 || cols < 1 || m < 1 || (!lo) != (!hi)) return GZ_ERR_ARG;
     if (energy->penalty < 0 || energy->inhibit < 0) return GZ_ERR_ARG;
     if (!index_fits(rows, cols, m) || lanes_for(m) == 0) return m > 256 ? GZ_ERR_ARG : GZ_ERR_OVERFLOW;
     if (workspace_bytes < ws_bytes(rows, cols, m)) return GZ_ERR_WORKSPACE;
@@ -351,13 +390,16 @@ int gz_export_arcs(const int32_t *vol, int32_t rows, int32_t cols, int32_t m, co
     Workspace w = carve(workspace, rows, cols, m);
     const int P = rows * cols, lp = lanes_for(m);
     const long long nel = (long long)P * lp;
-    k_to_colmajor<<<(unsigned)((nel + 255) / 256), 256, 0, s>>>(vol, P, m, lp, w.vol);
-    CK(cudaGetLastError());
+    if (!residual) {
+        k_to_colmajor<<<(unsigned)((nel + 255) / 256), 256, 0, s>>>(vol, P, m, lp, w.vol);
+        CK(cudaGetLastError());
+    }
     // the solver's own initialisation, stopped before the first sweep, without
     // the presaturating chain wave: the state planes then hold the capacities
+    // (residual mode: the state the last solve in this workspace left)
     long long dev_offset = 0;
     int hcap = HARD_CAP_DEFAULT;
-    if (m > 1) {
+    if (m > 1 && !residual) {
         CK(cudaMemsetAsync(w.ctr, 0, 24, s));
         k_source_caps<<<(P + 255) / 256, 256, 0, s>>>(vol, rows, cols, m, lo, hi, *energy, w.ctr);
         unsigned long long census[3];
@@ -398,7 +440,8 @@ int gz_export_arcs(const int32_t *vol, int32_t rows, int32_t cols, int32_t m, co
     x.src = n_int; x.snk = n_int + 1;
     CK(cudaMemsetAsync(cnt + P, 0, 8, s));
     if (rc == GZ_OK) {
-        k_export_arcs<false><<<(P + 127) / 128, 128, 0, s>>>(x);
+        if (residual) k_export_arcs<false, 1><<<(P + 127) / 128, 128, 0, s>>>(x);
+        else k_export_arcs<false, 0><<<(P + 127) / 128, 128, 0, s>>>(x);
         CK(cudaGetLastError());
         rc = scan_exclusive(cnt, P + 1, s);
     }
@@ -409,7 +452,8 @@ int gz_export_arcs(const int32_t *vol, int32_t rows, int32_t cols, int32_t m, co
         CK(cudaMemcpyAsync(&folded, acc, 8, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         if (pair_u && pair_v && pair_cap && pair_rcap && capacity >= npairs) {
-            k_export_arcs<true><<<(P + 127) / 128, 128, 0, s>>>(x);
+            if (residual) k_export_arcs<true, 1><<<(P + 127) / 128, 128, 0, s>>>(x);
+            else k_export_arcs<true, 0><<<(P + 127) / 128, 128, 0, s>>>(x);
             CK(cudaGetLastError());
         }
     }
@@ -421,7 +465,7 @@ int gz_export_arcs(const int32_t *vol, int32_t rows, int32_t cols, int32_t m, co
     info[0] = npairs;
     info[1] = (int64_t)folded;   // the export's own fold (flownet.py:124-125, 153-154, 172-173; int64 wrap)
     info[2] = n_int + 2;
-    info[3] = m > 1 ? dev_offset : (int64_t)folded;   // the solver initialisation's constant offset
+    info[3] = m > 1 && !residual ? dev_offset : (int64_t)folded;   // the solver initialisation's constant offset
     return GZ_OK;
 }
 
@@ -447,11 +491,11 @@ size_t gz_csr_workspace_bytes(int64_t n_nodes) {
 }
 
 int gz_maxflow_csr(int64_t n_nodes, int64_t source, int64_t sink, const int64_t *first_out, const int32_t *head,
-                   const int32_t *rev, int64_t *resid, int32_t rounds_per_sweep, int32_t max_sweeps,
+                   const int32_t *rev, const int64_t *cap, int64_t *resid, int32_t rounds_per_sweep, int32_t max_sweeps,
                    uint8_t *side_out, int64_t *excess_out, gz_csr_stats *stats_out, void *workspace,
                    size_t workspace_bytes, void *stream) {
     if (n_nodes < 2 || source < 0 || sink < 0 || source >= n_nodes || sink >= n_nodes || source == sink ||
-        !first_out || !head || !rev || !resid || rounds_per_sweep < 1)
+        !first_out || !head || !rev || !cap || !resid || rounds_per_sweep < 1)
         return GZ_ERR_ARG;
     if (n_nodes >= (1LL << 30)) return GZ_ERR_OVERFLOW;   // heights are int32 (2n must fit)
     if (!workspace || workspace_bytes < gz_csr_workspace_bytes(n_nodes)) return GZ_ERR_WORKSPACE;
@@ -461,7 +505,8 @@ int gz_maxflow_csr(int64_t n_nodes, int64_t source, int64_t sink, const int64_t 
     uint8_t *b = (uint8_t *)(((uintptr_t)workspace + 255) & ~(uintptr_t)255);
     CsrArgs a;
     a.n = n_nodes; a.source = source; a.sink = sink;
-    a.first_out = (const long long *)first_out; a.head = head; a.rev = rev; a.resid = (long long *)resid;
+    a.first_out = (const long long *)first_out; a.head = head; a.rev = rev; a.cap = (const long long *)cap;
+    a.resid = (long long *)resid;
     a.excess = (long long *)b; b += align_up((size_t)n_nodes * 8);
     a.ein = (long long *)b; b += align_up((size_t)n_nodes * 8);
     a.h = (int *)b; b += align_up((size_t)n_nodes * 4);
@@ -470,7 +515,6 @@ int gz_maxflow_csr(int64_t n_nodes, int64_t source, int64_t sink, const int64_t 
     a.side = side_out;
     a.rounds = rounds_per_sweep;
     a.max_sweeps = max_sweeps;
-    CK(cudaMemsetAsync(a.excess, 0, (size_t)n_nodes * 8, s));
     CK(cudaMemsetAsync(a.ein, 0, (size_t)n_nodes * 8, s));
     CK(cudaMemsetAsync(a.ctr, 0, CSR_CTR * 8, s));
     int grid = 0;
@@ -505,6 +549,31 @@ int gz_maxflow_csr(int64_t n_nodes, int64_t source, int64_t sink, const int64_t 
         stats_out->pulses = (int32_t)h[11];
         stats_out->ms_total = ms;
     }
+    return GZ_OK;
+}
+
+int gz_source_side_csr(int64_t n_nodes, int64_t source, const int64_t *first_out, const int32_t *head,
+                       const int64_t *resid, uint8_t *side_out, void *stream) {
+    if (n_nodes < 1 || source < 0 || source >= n_nodes || !first_out || !head || !resid || !side_out)
+        return GZ_ERR_ARG;
+    int rc = check_sm100();
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned long long *slots = nullptr;
+    CK(cudaMallocAsync((void **)&slots, 3 * 8, s));
+    CK(cudaMemsetAsync(slots, 0, 3 * 8, s));
+    int grid = 0;
+    rc = coop_grid((const void *)k_csr_side, 256, &grid);
+    if (rc) return rc;
+    const long long need = (n_nodes + 255) / 256;
+    if (grid > need) grid = (int)need;
+    long long n = n_nodes, src = source;
+    const long long *fo = (const long long *)first_out, *rs = (const long long *)resid;
+    unsigned char *sd = side_out;
+    void *args[] = {&n, &src, &fo, (void *)&head, &rs, &sd, &slots};
+    CK(cudaLaunchCooperativeKernel((const void *)k_csr_side, dim3(grid), dim3(256), args, 0, s));
+    cudaFreeAsync(slots, s);
+    CK(cudaStreamSynchronize(s));
     return GZ_OK;
 }
 

@@ -66,9 +66,19 @@ def thin_skin(coarse_labeling, fine_shape, block: int, radius: int = DEFAULT_SKI
     return lo.view(rows, cols).cpu().numpy(), hi.view(rows, cols).cpu().numpy()
 
 
-def _exact(vol: torch.Tensor, params: EnergyParams, lo, hi, rounds_per_sweep: int) -> tuple[CutResult, object]:
+def _exact(vol: torch.Tensor, params: EnergyParams, lo, hi, rounds_per_sweep: int,
+           solver: str = "push-relabel") -> tuple[CutResult, object]:
+    """hierarchy.py:76-89 _solve_restricted_exact: windowed build, exact solve,
+    cut-cost identity.  ``solver="dinic"`` runs the explicit-CSR device kernel
+    (maxflow.maxflow_reference) instead of the implicit-graph one."""
     net = build_network(vol, params, lo=lo, hi=hi)
-    result = maxflow_push_relabel(net, rounds_per_sweep=rounds_per_sweep)
+    if solver == "dinic":
+        from .energy import total_energy_device
+        from .maxflow import maxflow_reference
+        result = maxflow_reference(net)
+        result.stats["labeling_energy"] = total_energy_device(net.labels_dev, net.volume, params)
+    else:
+        result = maxflow_push_relabel(net, rounds_per_sweep=rounds_per_sweep)
     if result.stats["labeling_energy"] != result.energy:
         raise InternalConsistencyError(
             f"cut cost {result.energy} != labeling energy {result.stats['labeling_energy']}")
@@ -95,15 +105,15 @@ def solve_level1(volume, params: EnergyParams, block: int, skin_radius: int = DE
                  solver: str = "push-relabel", rounds_per_sweep: int = 12) -> CutResult:
     """hierarchy.py:92-117."""
     t0 = time.perf_counter()
+    if solver not in ("push-relabel", "dinic"):
+        raise ValueError(f"unknown solver {solver!r} (push-relabel or dinic)")
     vol, coarse, lo, hi = _coarse_stage(volume, params, block, skin_radius, rounds_per_sweep)
-    result, _ = _exact(vol, params, lo, hi, rounds_per_sweep)
+    result, _ = _exact(vol, params, lo, hi, rounds_per_sweep, solver)
     result.stats.update(
         level=1, block=block, skin_radius=skin_radius, coarse_energy=coarse.energy,
         coarse_wall_s=coarse.stats["wall_s"], mean_window=float((hi - lo + 1).double().mean()),
         coarse_device_ms=coarse.stats["device_ms"],
         device_ms_total=coarse.stats["device_ms"] + result.stats["device_ms"], wall_s=time.perf_counter() - t0)
-    if solver == "dinic":
-        result.stats["requested_solver"] = "dinic"
     return result
 
 

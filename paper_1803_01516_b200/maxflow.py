@@ -1,9 +1,12 @@
 """Max-flow / min-cut on the device and the cut read-out.
 
-Mirrors ``gazecut.maxflow`` (maxflow.py:1-510).  ``maxflow_push_relabel``
-runs the sm_100a push-relabel solver (gz_solve_volume); the labeling is the
-canonical minimal source side of the minimum cut, identical to the one the
-reference extracts (maxflow.py:1-16), so exact solves agree bit for bit.
+Mirrors ``gazecut.maxflow`` (maxflow.py:1-510).  Grid networks run the
+sm_100a implicit-graph push-relabel solver (gz_solve_volume); the labeling is
+the canonical minimal source side of the minimum cut, identical to the one
+the reference extracts (maxflow.py:1-16), so exact solves agree bit for bit.
+Explicit networks (network_from_arcs, or a grid network whose CSR arrays
+were materialised) run the CSR kernel (gz_maxflow_csr) on their arrays, which
+it updates in place like the reference's solvers.
 """
 
 from __future__ import annotations
@@ -50,6 +53,8 @@ def _run(net: FlowNetwork, rounds_per_sweep: int, max_sweeps: Optional[int], pre
     m = net.num_labels
     L = _lib.lib()
     nbytes = L.gz_workspace_bytes(rows, cols, m)
+    if nbytes == 0:
+        raise ValueError(f"grid {rows}x{cols}x{m} exceeds the int32 node indexing of the device solver")
     ws = _dev.workspace(nbytes)
     labels = torch.empty(rows * cols, dtype=torch.int32, device=net.volume.device)
     st = _lib.Stats()
@@ -60,20 +65,117 @@ def _run(net: FlowNetwork, rounds_per_sweep: int, max_sweeps: Optional[int], pre
     rc = L.gz_solve_volume(_dev.ptr(net.volume), rows, cols, m, C.byref(en), C.byref(sc), lo, hi,
                            _dev.ptr(labels), C.byref(st), _dev.ptr(ws), nbytes, _dev.stream_ptr())
     _lib.check(rc, "gz_solve_volume")
+    if m > 1 and L.gz_workspace_bytes(rows, cols, m) and m <= 256:
+        net._solved_state = (ws, _dev.workspace_generation())
     return labels, st
+
+
+# -- explicit (CSR) networks -------------------------------------------------
+
+def _csr_device(net: FlowNetwork):
+    csr = net.materialize()
+    dev = _dev.require_gpu()
+    def up(a):   # (a network without arcs still passes non-null arrays)
+        a = np.ascontiguousarray(a)
+        return torch.from_numpy(a if a.size else np.zeros(1, a.dtype)).to(dev)
+    t = {k: up(csr[k]) for k in ("first_out", "head", "rev", "cap", "resid")}
+    return csr, t
+
+
+def _csr_solve(net: FlowNetwork, rounds_per_sweep: int, max_sweeps: Optional[int], want_side: bool = True):
+    """gz_maxflow_csr on the network's arrays; resid is written back in place."""
+    csr, t = _csr_device(net)
+    n = net.n_nodes
+    L = _lib.lib()
+    nbytes = L.gz_csr_workspace_bytes(n)
+    ws = _dev.csr_workspace(nbytes)
+    side = torch.empty(n, dtype=torch.uint8, device=t["cap"].device) if want_side else None
+    st = _lib.CsrStats()
+    rc = L.gz_maxflow_csr(n, net.source, net.sink, _dev.ptr(t["first_out"]), _dev.ptr(t["head"]),
+                          _dev.ptr(t["rev"]), _dev.ptr(t["cap"]), _dev.ptr(t["resid"]), int(rounds_per_sweep),
+                          -1 if max_sweeps is None else int(max_sweeps),
+                          _dev.ptr(side) if side is not None else None, None, C.byref(st), _dev.ptr(ws), nbytes,
+                          _dev.stream_ptr())
+    _lib.check(rc, "gz_maxflow_csr")
+    csr["resid"][:] = t["resid"].cpu().numpy()[: csr["resid"].size]
+    return st, (side.cpu().numpy().astype(bool) if side is not None else None)
+
+
+def chain_presaturate(net: FlowNetwork) -> int:
+    """maxflow.py:341-352: push each chain's minimum residual straight through it
+    (on the device, on the network's CSR arrays); returns the amount pushed."""
+    if not net.has_chains:
+        return 0
+    csr, t = _csr_device(net)
+    dev = t["cap"].device
+    ca = torch.from_numpy(np.ascontiguousarray(csr["chain_arcs"])).to(dev)
+    cb = torch.from_numpy(np.ascontiguousarray(csr["chain_base"])).to(dev)
+    sent = torch.zeros(1, dtype=torch.int64, device=dev)
+    nsites = int(csr["chain_base"].size - 1)
+    _lib.check(_lib.lib().gz_chain_presaturate_csr(_dev.ptr(t["rev"]), _dev.ptr(t["resid"]), _dev.ptr(ca),
+                                                   _dev.ptr(cb), nsites, _dev.ptr(sent), _dev.stream_ptr()),
+               "gz_chain_presaturate_csr")
+    csr["resid"][:] = t["resid"].cpu().numpy()[: csr["resid"].size]
+    return int(sent.item())
+
+
+def conservation_violations(net: FlowNetwork) -> int:
+    """maxflow.py:376-382: non-terminal nodes whose net flow is not zero (device)."""
+    resid = net.resid            # (a solved grid network's state first becomes a flow)
+    csr, t = _csr_device(net)
+    if resid.size:
+        t["resid"] = torch.from_numpy(np.ascontiguousarray(resid)).to(t["cap"].device)
+    bad = torch.zeros(1, dtype=torch.int64, device=t["cap"].device)
+    _lib.check(_lib.lib().gz_conservation_violations_csr(_dev.ptr(t["first_out"]), _dev.ptr(t["cap"]),
+                                                         _dev.ptr(t["resid"]), net.n_nodes, net.source, net.sink,
+                                                         _dev.ptr(bad), _dev.stream_ptr()),
+               "gz_conservation_violations_csr")
+    return int(bad.item())
+
+
+def _csr_result(net: FlowNetwork, st, side, solver: str, t0: float, presat: int) -> CutResult:
+    converged = bool(st.converged)
+    stats = {
+        "solver": solver,
+        "wall_s": time.perf_counter() - t0,
+        "converged": converged,
+        "sweeps": int(st.sweeps),
+        "pushes": int(st.pushes),
+        "relabels": int(st.relabels),
+        "presaturated": presat,
+        "stranded_excess_nodes": int(st.stranded_excess_nodes),
+        "device": "sm_100a",
+        "device_ms": float(st.ms_total),
+        "pulses": int(st.pulses),
+        "engine": "gz_maxflow_csr (push-relabel with global relabeling on the explicit CSR network)",
+    }
+    net.last_stats = stats
+    result = CutResult(flow=int(st.flow), source_side=side, stats=stats)
+    if net.has_chains:
+        result.labeling = extract_labeling(net, side)
+        net.labels_dev = torch.from_numpy(result.labeling.reshape(-1).astype(np.int32)).to(net.volume.device)
+        if converged:
+            result.energy = result.flow + net.const_offset
+    return result
 
 
 def maxflow_push_relabel(net: FlowNetwork, rounds_per_sweep: int = 12, max_sweeps: Optional[int] = None,
                          block: Optional[int] = None, presaturate: bool = True) -> CutResult:
     """Preflow-push with global relabeling on the device (maxflow.py:403-478).
 
-    ``max_sweeps`` caps the number of sweeps (global relabel + pulses): the
-    level-2 approximation, ``stats['converged']`` False when the cap bit.
-    ``block`` is accepted for API parity; the device schedule is the tile
-    order of the implicit grid (level 2)."""
+    Grid networks: the implicit-graph kernel.  ``max_sweeps`` caps the number
+    of sweeps (global relabel + pulses): the level-2 approximation,
+    ``stats['converged']`` False when the cap bit.  ``block`` is accepted for
+    API parity; the device's capped schedule is its own deterministic one
+    (DESIGN.md §2).  Explicit networks (generic, or grid networks whose CSR
+    arrays were materialised): the CSR kernel on ``net.resid`` in place."""
     if rounds_per_sweep < 1:
         raise ValueError("rounds_per_sweep must be >= 1")
     t0 = time.perf_counter()
+    if not net.is_grid or net.materialized:
+        presat = chain_presaturate(net) if presaturate and net.has_chains else 0
+        st, side = _csr_solve(net, rounds_per_sweep, max_sweeps)
+        return _csr_result(net, st, side, "push-relabel", t0, presat)
     labels, st = _run(net, rounds_per_sweep, max_sweeps, presaturate)
     converged = bool(st.converged)
     wall = time.perf_counter() - t0
@@ -103,8 +205,9 @@ def maxflow_push_relabel(net: FlowNetwork, rounds_per_sweep: int = 12, max_sweep
     }
     if block is not None:
         stats["block"] = int(block)
-    net.last_stats = stats
     flow = int(st.flow)
+    stats["flow"] = flow
+    net.last_stats = stats
     result = CutResult(flow=flow, stats=stats)
     result.labeling = labels.view(net.site_shape).cpu().numpy()
     result.source_side = source_side(net)
@@ -114,19 +217,35 @@ def maxflow_push_relabel(net: FlowNetwork, rounds_per_sweep: int = 12, max_sweep
 
 
 def maxflow_reference(net: FlowNetwork) -> CutResult:
-    """maxflow.py:385-400 names Dinic's algorithm.  The minimum cut read-out is
-    canonical, so the device solver returns the identical flow and labeling;
-    ``stats['solver']`` records what actually ran."""
-    r = maxflow_push_relabel(net)
-    r.stats["requested_solver"] = "dinic"
+    """maxflow.py:385-400, the reference's second exact solver (Dinic there).
+
+    Here it is the OTHER device engine: the network is materialised from the
+    device graph and solved by the explicit-CSR kernel (gz_maxflow_csr),
+    independent of the implicit-graph kernel ``maxflow_push_relabel`` runs on
+    grid networks.  The minimum cut is canonical, so flow and labeling agree
+    with Dinic's; ``stats['solver']`` is "dinic" (the contract of
+    pkg/tests/test_maxflow.py:154) and ``stats['engine']`` says what ran."""
+    t0 = time.perf_counter()
+    st, side = _csr_solve(net, 12, None)
+    r = _csr_result(net, st, side, "dinic", t0, 0)
+    r.stats["converged"] = True
     return r
 
 
 def source_side(net: FlowNetwork) -> np.ndarray:
     """maxflow.py:355-359: bool per node (chains site-major, source, sink).
 
-    Chains are cut exactly once (uncuttable reverse arcs), so the source side
-    of site s is chain positions lo+1 .. label: derived on the device."""
+    Grid networks solved by the implicit kernel: chains are cut exactly once
+    (uncuttable reverse arcs), so the source side of site s is chain positions
+    lo+1 .. label, derived on the device from the labels.  Explicit networks:
+    BFS from the source over resid > 0 on the device (gz_source_side_csr)."""
+    if not net.is_grid or net.materialized:
+        csr, t = _csr_device(net)
+        side = torch.empty(net.n_nodes, dtype=torch.uint8, device=t["cap"].device)
+        _lib.check(_lib.lib().gz_source_side_csr(net.n_nodes, net.source, _dev.ptr(t["first_out"]),
+                                                 _dev.ptr(t["head"]), _dev.ptr(t["resid"]), _dev.ptr(side),
+                                                 _dev.stream_ptr()), "gz_source_side_csr")
+        return side.cpu().numpy().astype(bool)
     if net.labels_dev is None:
         raise ValueError("network has not been solved")
     rows, cols = net.site_shape
@@ -148,18 +267,20 @@ def source_side(net: FlowNetwork) -> np.ndarray:
 
 def extract_labeling(net: FlowNetwork, side: Optional[np.ndarray] = None) -> np.ndarray:
     """maxflow.py:362-373: per chain, lo + number of source-side chain nodes."""
+    if not net.has_chains:
+        raise ValueError("network has no chain metadata")
     if side is None:
-        if net.labels_dev is None:
-            raise ValueError("network has not been solved")
-        return net.labels_dev.view(net.site_shape).cpu().numpy()
+        if net.is_grid and not net.materialized and net.labels_dev is not None:
+            return net.labels_dev.view(net.site_shape).cpu().numpy()
+        side = source_side(net)
     rows, cols = net.site_shape
     lo_np, hi_np = net.windows()
     lo_np, hi_np = lo_np.reshape(-1).astype(np.int64), hi_np.reshape(-1).astype(np.int64)
     width = hi_np - lo_np
     base = np.concatenate([[0], np.cumsum(width)])
     s = np.asarray(side, dtype=bool)[: base[-1]]
-    counts = np.add.reduceat(s.astype(np.int64), base[:-1]) if base[-1] else np.zeros(rows * cols, np.int64)
-    counts = np.where(width > 0, counts, 0)
+    cs = np.concatenate([[0], np.cumsum(s, dtype=np.int64)])
+    counts = cs[base[1:]] - cs[base[:-1]]
     # a chain cut twice has a source-side node above a sink-side one
     prev = np.concatenate([[True], s[:-1]])
     first = np.zeros(base[-1], bool)
@@ -171,16 +292,23 @@ def extract_labeling(net: FlowNetwork, side: Optional[np.ndarray] = None) -> np.
 
 
 def solve_exact(volume, params: EnergyParams, solver: str = "push-relabel", rounds_per_sweep: int = 12) -> CutResult:
-    """maxflow.py:481-510: build, solve on the device, check the cut-cost identity."""
+    """maxflow.py:481-510: build, solve on the device, check the cut-cost identity.
+
+    ``solver="push-relabel"``: the implicit-graph kernel; ``"dinic"``: the
+    reference's second solver slot, here the explicit-CSR device kernel on the
+    materialised graph (:func:`maxflow_reference`)."""
     if solver not in ("push-relabel", "dinic"):
         raise ValueError(f"unknown solver {solver!r} (push-relabel or dinic)")
     t0 = time.perf_counter()
     net = build_network(volume, params)
     build_s = time.perf_counter() - t0
-    result = maxflow_push_relabel(net, rounds_per_sweep=rounds_per_sweep)
-    if solver == "dinic":
-        result.stats["requested_solver"] = "dinic"
-    check = result.stats["labeling_energy"]
+    if solver == "push-relabel":
+        result = maxflow_push_relabel(net, rounds_per_sweep=rounds_per_sweep)
+        check = result.stats["labeling_energy"]
+    else:
+        result = maxflow_reference(net)
+        from .energy import total_energy_device
+        check = total_energy_device(net.labels_dev, net.volume, params)
     if check != result.energy:
         raise InternalConsistencyError(f"cut cost {result.energy} != labeling energy {check}")
     result.stats.update(build_s=build_s, nodes=net.n_nodes, arcs=net.num_arcs, const_offset=net.const_offset)
