@@ -45,10 +45,10 @@ class _PRStats(C.Structure):
 
 def build_lib(force: bool = False) -> Path:
     """Compile gz_oracle.c with gcc (no GPU, no reference needed)."""
-    src = HERE / "gz_oracle.c"
-    if force or not LIB_PATH.exists() or LIB_PATH.stat().st_mtime < src.stat().st_mtime:
+    srcs = [HERE / "gz_oracle.c", HERE / "gz_certify.c"]
+    if force or not LIB_PATH.exists() or any(LIB_PATH.stat().st_mtime < s.stat().st_mtime for s in srcs):
         subprocess.run(
-            ["gcc", "-O2", "-shared", "-fPIC", "-std=c11", "-o", str(LIB_PATH), str(src)],
+            ["gcc", "-O2", "-shared", "-fPIC", "-std=c11", "-o", str(LIB_PATH), *map(str, srcs)],
             check=True,
         )
     return LIB_PATH
@@ -382,3 +382,26 @@ def error_count(labeling, depth, valid, tail=9):
     diff = np.abs(np.asarray(labeling, np.int64) - np.asarray(depth, np.int64))[np.asarray(valid, bool)]
     hist = np.bincount(np.minimum(diff, tail), minlength=tail + 1)
     return int(diff.sum()), int(diff.size), hist.astype(np.int64)
+
+
+CERTIFY_CHECKS = {1: "capacity bounds", 2: "conservation", 3: "flow value", 4: "cut cost",
+                  5: "minimal source side", 6: "out of memory"}
+
+
+def certify(vol, penalty, inhibit, planes: dict, labels, device_flow):
+    """oracle/gz_certify.c: the device state is a feasible maximum preflow whose
+    value equals the labeling's cut cost, and the labeling is the minimal source
+    side.  planes: int32 (P, m-1) arrays keyed cu, ph, pv,
+    dar, dbr, dad, dbd, e.  Returns (failed check or 0, report dict)."""
+    vol = np.ascontiguousarray(vol, dtype=np.int32)
+    rows, cols, m = vol.shape
+    arrs = [np.ascontiguousarray(planes[k], dtype=np.int32) for k in ("cu", "ph", "pv", "dar", "dbr", "dad", "dbd", "e")]
+    lab = np.ascontiguousarray(labels, dtype=np.int32)
+    rep = np.zeros(8, np.int64)
+    f = lib().gzc_certify
+    f.restype = C.c_int
+    f.argtypes = [C.c_int, C.c_int, C.c_int, _p, C.c_int32, C.c_int32] + [_p] * 9 + [_i64, _p]
+    rc = int(f(rows, cols, m, _ptr(vol), int(penalty), int(inhibit), *[_ptr(a) for a in arrs], _ptr(lab),
+               int(device_flow), _ptr(rep)))
+    keys = ("sink_inflow", "labeling_energy", "reached", "first_bad", "label_mismatches", "excess_nodes")
+    return rc, dict(zip(keys, (int(x) for x in rep[:6])))

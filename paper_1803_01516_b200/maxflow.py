@@ -70,6 +70,35 @@ def _run(net: FlowNetwork, rounds_per_sweep: int, max_sweeps: Optional[int], pre
     return labels, st
 
 
+_PLANES = (("cu", _lib.GZ_PLANE_CHAIN), ("ph", _lib.GZ_PLANE_SAME_RIGHT), ("pv", _lib.GZ_PLANE_SAME_DOWN),
+           ("dar", _lib.GZ_PLANE_DIAG_RIGHT), ("dbr", _lib.GZ_PLANE_DIAG_LEFT), ("dad", _lib.GZ_PLANE_DIAG_DOWN),
+           ("dbd", _lib.GZ_PLANE_DIAG_UP), ("e", _lib.GZ_PLANE_EXCESS), ("h", _lib.GZ_PLANE_HEIGHT))
+
+
+def solve_state(net: FlowNetwork, planes=("cu", "ph", "pv", "dar", "dbr", "dad", "dbd", "e")) -> dict:
+    """The final device state of the last implicit-graph solve of ``net``
+    (gz_export_state): int32 host arrays (sites, m-1), position t in column
+    t-1 -- the residual preflow the optimality certificate checks
+    (oracle/gz_certify.c).  Must be called before any other
+    device call reuses the solver workspace."""
+    if net._solved_state is None:
+        raise ValueError("network has no implicit-solve state (solve it with maxflow_push_relabel first)")
+    ws, gen = net._solved_state
+    if gen != _dev.workspace_generation():
+        raise RuntimeError("the solve state was overwritten by a later device call; re-solve the network")
+    rows, cols = net.site_shape
+    m = net.num_labels
+    out = {}
+    buf = torch.empty((rows * cols, m - 1), dtype=torch.int32, device=net.volume.device)
+    for name, plane in _PLANES:
+        if name not in planes:
+            continue
+        _lib.check(_lib.lib().gz_export_state(_dev.ptr(ws), rows, cols, m, plane, _dev.ptr(buf), _dev.stream_ptr()),
+                   "gz_export_state")
+        out[name] = buf.cpu().numpy()
+    return out
+
+
 # -- explicit (CSR) networks -------------------------------------------------
 
 def _csr_device(net: FlowNetwork):
