@@ -47,21 +47,27 @@ def state_bytes(rows: int, cols: int, m: int) -> int:
     return 8 * n_int + 4 * sites * m + 2 * nb * (m - 1) + 2 * nb * 2 * (m - 2)
 
 
-def solve_bytes(st: dict, rows: int, cols: int, m: int) -> int:
-    """Algorithmic bytes of one solve, phase by phase:
-    a push/relabel node update moves 2S/N_int bytes (47.4 B at
-    C1), counted only for the chains a pulse actually processed
-    (stats['node_updates'], counted on the device); a mask build reads the
-    state once and writes 13 arc-mask words + 1 excess word per site; a
-    bit-parallel BFS level reads 13 mask words + frontier + visited and writes
-    frontier + visited (68 B/site); a reach pass reads 12 neighbour mask words +
-    5 prefix words + 1 chain mask and writes 1 word (76 B/site)."""
+def update_bytes(st: dict, rows: int, cols: int, m: int) -> int:
+    """SURVEY.md 8(d) algorithmic bytes of one solve: every graph-node update
+    (one interior node processed by one push/relabel pulse; counted on the
+    device, stats['node_updates']) moves 2S / N_int bytes, S the minimal state
+    (47.4 B at C1).  This is the figure roofline.achieved uses."""
+    S = state_bytes(rows, cols, m)
+    n_int = rows * cols * (m - 1)
+    return int(st["node_updates"] * 2 * S / n_int)
+
+
+def other_bytes(st: dict, rows: int, cols: int, m: int) -> int:
+    """Work outside the push/relabel pulses, reported beside (not inside) the
+    roofline: a mask build reads the state once and
+    writes 13 arc-mask words + 1 excess word per site; a bit-parallel BFS level
+    reads 13 mask words + frontier + visited and writes frontier + visited
+    (68 B/site; temporally blocked, so most of it stays in shared memory); a
+    reach pass moves 76 B/site."""
     S = state_bytes(rows, cols, m)
     sites = rows * cols
-    n_int = sites * (m - 1)
     builds = st["sweeps"] + 1
-    return int(st["node_updates"] * 2 * S / n_int + builds * (S + 56 * sites) + st["bfs_passes"] * 68 * sites
-               + st["reach_passes"] * 76 * sites)
+    return int(builds * (S + 56 * sites) + st["bfs_passes"] * 68 * sites + st["reach_passes"] * 76 * sites)
 
 
 def rank_seeds(rank: int, pairs_per_step: int, steps: int) -> list[int]:
@@ -177,6 +183,18 @@ def run_reference(args, rank: int, world: int):
     tiny = np.arange(2 * 3 * 4, dtype=np.int64).reshape(2, 3, 4)
     for _ in range(args.warmup):   # native code: warm-up = loading + page-in, kept tiny
         o.solve_exact(tiny, 1, 5)
+    # one pair on one core, stage by stage (the 1-core latency split)
+    from paper_1803_01516_b200 import cuboid_from_disparity_range
+    cub = cuboid_from_disparity_range(W_IMG, H_IMG, DIS_MIN, DIS_MAX, num_labels=LABELS)
+    (l1,), (r1,) = scenes([100])
+    t0 = time.perf_counter()
+    vol = o.sad_volume(l1, r1, cub.g_min, cub.g_extent, cub.y_min, cub.y_extent, cub.d_min, LABELS)
+    t1 = time.perf_counter()
+    o.solve_exact(vol, PENALTY, INHIBIT)
+    t2 = time.perf_counter()
+    lat = {"sad_volume": t1 - t0, "solve_exact": t2 - t1, "total": t2 - t0,
+           "ms_per_pair": 1000 * (t2 - t0), "seed": 100, "threads": 1}
+    log(f"[reference] 1-core latency: {lat}")
     rates, walls = [], []
     for k in range(args.steps):
         rate, wall, flows = cpu_baseline_sample(n, list(range(100 + k * n, 100 + (k + 1) * n)))
@@ -195,6 +213,7 @@ def run_reference(args, rank: int, world: int):
                          "sample": f"{n} pairs per step, one per host thread (oracle/gz_oracle.c, C port of "
                                    "sad_volume + solve_exact)"},
         "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "latency_1core_s": lat,
     }
     print(json.dumps(line), flush=True)
 
@@ -204,8 +223,10 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--pairs", type=int, default=64,
-                    help="pairs per rank per step (64: N=8 ranks solve BASELINE config 4's 512-pair batch per step)")
+    ap.add_argument("--pairs", type=int, default=1184,
+                    help="pairs per rank per step (1184 = 8 per team of the batched launch; BASELINE config 4 "
+                         "is a 512-pair batch)")
+    ap.add_argument("--no-lone", action="store_true", help="skip the lone-pair latency measurement")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=32)
@@ -298,45 +319,67 @@ def main():
 
     # ---- roofline of the solve kernel ----
     S = state_bytes(cub.y_extent, cub.g_extent, LABELS)
-    n_int = cub.y_extent * cub.g_extent * (LABELS - 1)
-    alg = [solve_bytes(st, cub.y_extent, cub.g_extent, LABELS) for st in all_stats]
+    upd = [update_bytes(st, cub.y_extent, cub.g_extent, LABELS) for st in all_stats]
+    oth = [other_bytes(st, cub.y_extent, cub.g_extent, LABELS) for st in all_stats]
     kern_ms = [st["device_ms"] for st in all_stats]
-    # Several solve launches run concurrently (each on 1/k of the SMs), so the
-    # kernel's achieved bandwidth is the algorithmic bytes of every launch in the
-    # timed region over the region's device time (this rank); the per-launch
-    # figure (bytes / own event time) is reported beside it.
+    # one kernel launch per step solves the whole batch (batched teams), so the
+    # step's device time is the kernel's; achieved = node-update bytes / time
     dev_s = sum(step_ms) / 1000.0
-    achieved = sum(alg) / dev_s / 1e9
-    per_launch = sum(alg) / (sum(kern_ms) / 1000.0) / 1e9
+    achieved = sum(upd) / dev_s / 1e9
     gnups = sum(st["node_updates"] for st in all_stats) / dev_s / 1e9
     peaks_path = ROOT / "MEASURED_PEAKS.json"
     if peaks_path.exists():
-        peak, peak_src = float(json.loads(peaks_path.read_text())["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+        peak, peak_src = float(json.loads(peaks_path.read_text())["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
     else:
         peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    l2 = None
+    l2_path = ROOT / "profiles" / "l2_peak.json"
+    if l2_path.exists():
+        l2_peak = float(json.loads(l2_path.read_text())["l2_read_gbs"])
+        l2 = {"peak": l2_peak, "achieved": achieved, "frac": achieved / l2_peak, "unit": "GB/s",
+              "peak_source": "profiles/l2_peak.json (tools/micro/l2_bench.cu, measured)"}
     traffic = None
     tr_path = ROOT / "profiles" / "traffic.json"
     if tr_path.exists():
-        traffic = json.loads(tr_path.read_text()).get("dram_bytes_per_launch")   # from the committed ncu capture
+        traffic = json.loads(tr_path.read_text()).get("dram_bytes_per_pair")   # from the committed ncu capture
+
+    # ---- lone-pair latency (the metric's ms per pair): C1 seeds 0-7, one at a time on all SMs ----
+    lone = []
+    if not args.no_lone:
+        for sd in range(8):
+            sc = gz.make_scene(sd, W_IMG, H_IMG, DIS_MIN, DIS_MAX)
+            vol = gz.sad_volume_device(sc.left, sc.right, cub)
+            gz.solve_exact(vol, params)   # warm-up of the lone instance
+            lone.append(gz.solve_exact(vol, params).stats["device_ms"])
 
     line = {
         "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "ms_per_pair": max_ms / (P * args.steps),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
         "data": "synthetic (make_scene seeds, bit-identical to the reference generator)",
-        "config": {"workload": "C4-shaped: Tsukuba 384x288x16 pairs, exact solve (sad_volume + solve_exact)",
+        "config": {"workload": "C4-shaped: batches of Tsukuba 384x288x16 pairs, exact solve (sad_volume + "
+                               "solve_exact) per pair; batched teams of GZ_PAIR_TEAM CTAs in one launch",
                    "pairs_per_rank_per_step": P, "image": f"{W_IMG}x{H_IMG}x3", "labels": LABELS,
                    "penalty": PENALTY, "inhibit": INHIBIT, "parallelism": f"pair-sharded x{world}",
                    "l2": "256 MiB buffer written between timed steps (L2 flush)"},
         "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": int(lh[batch(0)].nbytes * 2),
                 "d2h_bytes_per_step": int(lab_host.nbytes)},
-        "gpu_launches": 2 * P * args.steps,
+        "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "gz4::gz_tilesolve_kernel", "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": statistics.mean(alg), "state_bytes_S": S,
-                     "mean_launch_ms": statistics.mean(kern_ms), "per_launch_achieved": per_launch,
-                     "concurrent_launches": min(16, int(os.environ.get("GZ_PAIR_CONC", "8"))),
-                     "note": "state (S = 38 MB) is L2-resident; the kernel is barrier/latency bound (DESIGN.md)"},
+                     "traffic": traffic, "kernel": "gz4::gz_pairs_kernel (one launch per step, batched teams)",
+                     "peak_source": peak_src,
+                     "achieved_definition": "SURVEY 8(d): device node_updates x 2S/N_int bytes / step device time",
+                     "bytes_per_node_update": 2 * S / (cub.y_extent * cub.g_extent * (LABELS - 1)),
+                     "node_update_bytes_per_pair": statistics.mean(upd), "state_bytes_S": S,
+                     "other_bytes_per_pair": statistics.mean(oth),
+                     "other_bytes_note": "mask builds, BFS levels, reach passes (DESIGN.md section 4); not in achieved",
+                     "l2": l2,
+                     "limiter": "latency: dependent L2/HBM round trips per group update and per BFS tile round "
+                                "(ncu: profiles/)",
+                     "mean_pair_device_ms": statistics.mean(kern_ms)},
+        "lone_pair_ms": ({"seeds": "0-7", "mean": statistics.mean(lone), "min": min(lone), "max": max(lone),
+                          "each": [round(x, 3) for x in lone], "note": "one pair at a time on all SMs (solve_exact)"}
+                         if lone else None),
         "gnups": gnups,
         "clocks": clocks.summary(),
         "wall_s_timed_region": wall_s,
@@ -348,9 +391,15 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         n = min(host_threads(), args.cpu_threads)
         rate, wall, flows = cpu_baseline_sample(n, seeds)
+        # the same pairs on the device: the baseline's flows double as a parity check
+        _, gst = solver.solve(left_d[:n], right_d[:n])
+        gflows = [st["flow"] for st in gst]
+        if gflows != flows:
+            raise SystemExit(f"parity failure: device flows {gflows} != oracle flows {flows}")
         line["cpu_baseline"] = {"value": rate, "unit": "pairs/s", "cores": n, "kind": "port",
                                 "sample": f"{n} C1 pairs, one per host thread, {wall:.1f} s wall "
-                                          "(oracle/gz_oracle.c: sad_volume + solve_exact)"}
+                                          "(oracle/gz_oracle.c: sad_volume + solve_exact)",
+                                "parity": f"{n}/{n} device flows equal the oracle's"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -117,13 +117,23 @@ int gz_solve_volume(const int32_t *vol, int32_t rows, int32_t cols, int32_t m, c
  * back to back (left/right: batch x height x width x channels uint8).
  * labels_out: batch x (y_extent, g_extent) int32; stats_out: batch entries
  * (host memory).  workspace: k * gz_workspace_bytes(y_extent, g_extent, m)
- * runs up to k pair solves at once (k <= 8, env GZ_PAIR_CONC), each
- * a cooperative launch over 1/k of the SMs on its own stream; at least one
- * workspace is required. */
+ * runs up to k pair solves at once.  m <= 16 (BASELINE config 4): ONE launch
+ * of teams of GZ_PAIR_TEAM (2) CTAs, team k on workspace slice k, pairs handed
+ * out by a device queue (gz4::gz_pairs_kernel; size the workspace with
+ * gz_pairs_workspace_bytes).  Otherwise up to GZ_PAIR_CONC (8) cooperative
+ * launches over 1/k of the SMs each, one stream per slice.  At least one
+ * slice is required.  Calls on one device are serialised (a per-device lock
+ * guards the stream pool and the pinned counter buffer). */
 int gz_solve_pairs(const uint8_t *left, const uint8_t *right, int32_t batch, int32_t img_h, int32_t img_w,
                    int32_t channels, const gz_cuboid *cuboid, const gz_energy *energy, const gz_sched *sched,
                    int32_t *labels_out, gz_stats *stats_out, void *workspace, size_t workspace_bytes,
                    void *stream);
+
+/* Workspace for gz_solve_pairs to keep as many pairs of `batch` in flight as
+ * the device runs at once (m <= 16: one workspace slice per team of the
+ * batched launch, GZ_PAIR_TEAM CTAs per team; otherwise GZ_PAIR_CONC slices).
+ * Queries the current device; 0 on error. */
+size_t gz_pairs_workspace_bytes(int32_t rows, int32_t cols, int32_t m, int32_t batch);
 
 /* Same as gz_solve_pairs with HOST buffers (pinned or pageable): copies in,
  * solves, copies labels out.  The reference-facing end-to-end call. */

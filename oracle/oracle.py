@@ -45,7 +45,7 @@ class _PRStats(C.Structure):
 
 def build_lib(force: bool = False) -> Path:
     """Compile gz_oracle.c with gcc (no GPU, no reference needed)."""
-    srcs = [HERE / "gz_oracle.c", HERE / "gz_certify.c"]
+    srcs = [HERE / "gz_oracle.c", HERE / "gz_certify.c", HERE / "gz_capped.c"]
     if force or not LIB_PATH.exists() or any(LIB_PATH.stat().st_mtime < s.stat().st_mtime for s in srcs):
         subprocess.run(
             ["gcc", "-O2", "-shared", "-fPIC", "-std=c11", "-o", str(LIB_PATH), *map(str, srcs)],
@@ -405,3 +405,23 @@ def certify(vol, penalty, inhibit, planes: dict, labels, device_flow):
                int(device_flow), _ptr(rep)))
     keys = ("sink_inflow", "labeling_energy", "reached", "first_bad", "label_mismatches", "excess_nodes")
     return rc, dict(zip(keys, (int(x) for x in rep[:6])))
+
+
+def capped_schedule(volume, penalty, inhibit, lo, hi, K, max_sweeps, bfs_min, H, presaturate=True):
+    """oracle/gz_capped.c: the device's deterministic capped (level-2) schedule
+    restated on the CPU.  Returns (labels (rows, cols) int32, report dict)."""
+    vol = np.ascontiguousarray(volume, dtype=np.int32)
+    rows, cols, m = vol.shape
+    lo_a = np.ascontiguousarray(np.asarray(lo, dtype=np.int32).reshape(rows * cols))
+    hi_a = np.ascontiguousarray(np.asarray(hi, dtype=np.int32).reshape(rows * cols))
+    if int((hi_a - lo_a).max(initial=0)) > 63:
+        raise ValueError("windows wider than 63 positions are not restated")
+    lab = np.empty(rows * cols, np.int32)
+    rep = np.zeros(4, np.int64)
+    f = lib().gzo_capped
+    f.restype = C.c_int
+    f.argtypes = [_p, C.c_int, C.c_int, C.c_int, C.c_int32, C.c_int32, _p, _p, C.c_int, C.c_int, C.c_int, C.c_int,
+                  C.c_int, _p, _p]
+    f(_ptr(vol), rows, cols, m, int(penalty), int(inhibit), _ptr(lo_a), _ptr(hi_a), int(K), int(max_sweeps),
+      int(bfs_min), int(H), 1 if presaturate else 0, _ptr(lab), _ptr(rep))
+    return lab.reshape(rows, cols), dict(zip(("flow", "sweeps", "pulses", "converged"), (int(x) for x in rep)))

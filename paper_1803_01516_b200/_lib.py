@@ -101,6 +101,8 @@ def lib():
         L.gz_solve_pairs.argtypes = [_vp, _vp, _i32, _i32, _i32, _i32, C.POINTER(Cuboid),
                                      C.POINTER(Energy), C.POINTER(Sched), _vp, C.POINTER(Stats),
                                      _vp, C.c_size_t, _vp]
+        L.gz_pairs_workspace_bytes.restype = C.c_size_t
+        L.gz_pairs_workspace_bytes.argtypes = [_i32, _i32, _i32, _i32]
         L.gz_solve_pairs_host.restype = C.c_int
         L.gz_solve_pairs_host.argtypes = L.gz_solve_pairs.argtypes
         L.gz_solve_volume_banded.restype = C.c_int
@@ -159,7 +161,7 @@ def check(status: int, where: str) -> None:
 
 # Every symbol include/gazecut_b200.h declares (checked by tests/test_abi.py).
 EXPORTED = (
-    "gz_workspace_bytes", "gz_sad_volume", "gz_solve_volume", "gz_solve_pairs",
+    "gz_workspace_bytes", "gz_sad_volume", "gz_solve_volume", "gz_solve_pairs", "gz_pairs_workspace_bytes",
     "gz_solve_pairs_host", "gz_solve_volume_banded", "gz_ground_truth_to_depth",
     "gz_error_count", "gz_render_disparity", "gz_solve_volume_batch", "gz_total_energy", "gz_coarsen", "gz_thin_skin",
     "gz_status_string", "gz_build_info", "gz_export_arcs", "gz_export_state", "gz_csr_workspace_bytes",

@@ -181,6 +181,31 @@ struct TailQ {
         const unsigned k = atomicAdd(n, 1u);
         if ((int)k < cap) q[k] = grp;
     }
+    // Warp-aggregated append (one band or the shared-memory tail list): every
+    // lane of the warp calls it with its number of entries; ONE atomic per warp
+    // reserves them all.  Returns this lane's first slot.
+    __device__ __forceinline__ bool aggregated() const { return !rt || rt->nbands == 1; }
+    __device__ __forceinline__ int reserve_warp(int cnt) const {
+        const int lane = threadIdx.x & 31;
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        unsigned base = 0u;
+        if (lane == 0 && total) base = atomicAdd(rt ? rt->cnt : n, (unsigned)total);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        return (int)base + incl - cnt;
+    }
+    __device__ __forceinline__ void store(int k, int grp) const {
+        if (rt) {
+            if (k < rt->nw * rt->P) rt->list[k] = grp;
+        } else if (k < cap) {
+            q[k] = grp;
+        }
+    }
 };
 
 // Residuals of the 14 arcs of a lane's node, target heights and kinds.
@@ -548,9 +573,17 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
     const int phL_d = dd[A_SL], pvU_d = dd[A_SU], dbrL_d = dd[A_DL], dbdU_d = dd[A_DU];
     const int dbr_up_d = -dd[A_UR], darL_up_d = -dd[A_UL], dbd_up_d = -dd[A_UD], dadU_up_d = -dd[A_UU];
     const int dn = dd[A_DN];
+    // Every inbox add and inbox-bit OR of this node is issued before any result
+    // is used (one memory round trip for all of them); the target groups that
+    // go on the worklist are appended after the write-back with one
+    // warp-aggregated atomic (TailQ::reserve_warp) instead of one returning
+    // atomic per push.
+    uint32_t lmask = 0u;            // bit jj: lateral push along arc jj into a real node
+    uint32_t olds[A_COUNT];
 #pragma unroll
     for (int jj = A_SR; jj <= A_DN; ++jj) {
         const int d = dd[jj];
+        olds[jj] = 0u;
         if (d <= 0) continue;
         pushed = true;
         ++pushes;
@@ -559,8 +592,11 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
         int site, pos;
         lateral_target(L, jj, site, pos);
         gz_atomic_add(p, &ein_cur[site * LPT + pos - 1], d);
-        const uint32_t o_ = gz_atomic_or(p, &IN_cur[((pos - 1) >> 5) * P + site], 1u << ((pos - 1) & 31));
-        if (tq && !(o_ && tq->dedupe)) tq->push(LP == 16 ? site >> 1 : ((pos - 1) / LP) * P + site);
+        uint32_t *inw = &IN_cur[((pos - 1) >> 5) * P + site];
+        const uint32_t bit = 1u << ((pos - 1) & 31);
+        if (tq) olds[jj] = gz_atomic_or(p, inw, bit);
+        else gz_atomic_or(p, inw, bit);
+        lmask |= 1u << jj;
     }
     // chain-down pushes arrive at lane j-1 (adds to its excess and to its chain-up
     // residual); out of a segment's first lane they cross into the segment below
@@ -637,8 +673,33 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
             if (DETPUSH) b.RL[L.wi] = rl;
         }
     }
-    if (tq && __any_sync(FULL, newA != 0u) && (threadIdx.x & 31) == 0)
-        tq->push(LP == 16 ? c_base >> 1 : L.wi);
+    if (tq) {
+        // worklist: the groups pushed into (a push into an inbox word already set
+        // this pulse is skipped with dedupe: that word's first push listed the
+        // group) and this group if it stays active
+        uint32_t want = 0u;
+#pragma unroll
+        for (int jj = A_SR; jj < A_DN; ++jj)
+            if (((lmask >> jj) & 1u) && !(olds[jj] && tq->dedupe)) want |= 1u << jj;
+        const bool self = __any_sync(FULL, newA != 0u) && (threadIdx.x & 31) == 0;
+        auto gid = [&](int jj) {
+            int site, pos;
+            lateral_target(L, jj, site, pos);
+            return LP == 16 ? site >> 1 : ((pos - 1) / LP) * P + site;
+        };
+        if (tq->aggregated()) {
+            int k = tq->reserve_warp(__popc(want) + (self ? 1 : 0));
+#pragma unroll
+            for (int jj = A_SR; jj < A_DN; ++jj)
+                if ((want >> jj) & 1u) tq->store(k++, gid(jj));
+            if (self) tq->store(k, LP == 16 ? c_base >> 1 : L.wi);
+        } else {
+#pragma unroll
+            for (int jj = A_SR; jj < A_DN; ++jj)
+                if ((want >> jj) & 1u) tq->push(gid(jj));
+            if (self) tq->push(LP == 16 ? c_base >> 1 : L.wi);
+        }
+    }
     // a push changes this site's residuals and the pair state / excess of its
     // neighbours: all their segments need their arc masks rebuilt next sweep
     const uint32_t pm = seg_ballot<LP>(pushed);

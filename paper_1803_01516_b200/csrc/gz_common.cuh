@@ -48,5 +48,7 @@ const void *kernel_for(int LP, int R, bool win, int occ, int rw);
 const void *kernels_lp16(bool win, int occ, int rw);
 const void *kernels_lp32(int R, bool win);
 const void *kernels_lp32w(int R, bool win);
+// the batched pair-solve kernel (gz_pairs_kernel) for 16-lane chains, occupancy 1 or 2
+const void *pairs_kernel_lp16(int occ);
 
 }  // namespace gz4

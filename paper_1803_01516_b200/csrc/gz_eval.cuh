@@ -180,7 +180,7 @@ int gz_solve_volume_batch(const int32_t *vol, int32_t rows, int32_t cols, int32_
     if ((unsigned long long)hcap_hard + census[0] >= 0x7fffffffull) hcap_hard = 0;
     int conc = 8;
     if (const char *cs = getenv("GZ_PAIR_CONC")) conc = atoi(cs);
-    if (conc > 16) conc = 16;
+    if (conc > DevicePool::MAX_STREAMS) conc = DevicePool::MAX_STREAMS;
     if ((size_t)conc * one > workspace_bytes) conc = (int)(workspace_bytes / one);
     if (conc > n) conc = n;
     if (conc < 1) conc = 1;

@@ -78,6 +78,7 @@ struct Prob {
     unsigned long long *ctr;  // counters, see CTR_*
     int sys;                  // row bands spanning GPUs: system-scope global atomics (gz_atomic_*)
     int init_only;            // stop after the initialisation (graph export, gz_export_arcs)
+    int tail_groups;          // one-CTA teams: enter the shared-memory tail mode at <= this many active groups
 };
 
 // Global-memory atomics of the v4 solver that can land in another GPU's band
@@ -102,6 +103,8 @@ enum Ctr : int {
     CTR_TRACE = 35,     // debug trace accumulator (GZ_TRACE=2)
     CTR_TQN = 36,       // tail-mode global worklist length
     CTR_ABORT = 37,     // multi-launch (row-band) team gave up waiting at a barrier
+    CTR_NS = 38,        // batched pair solves: device time of the pair (ns, %globaltimer)
+    CTR_PAIR = 39,      // batched pair solves: the pair a team is working on
     CTR_UPDATES = 30,   // node updates performed by pulses (v4)
     CTR_BAR0 = 32,      // 3 rotating team-barrier words (v4)
     CTR_COUNT = 40

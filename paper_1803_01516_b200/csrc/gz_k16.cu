@@ -11,4 +11,8 @@ const void *kernels_lp16(bool win, int occ, int rw) {
     return win ? (const void *)gz_tilesolve_kernel<16, 1, true, 1> : (const void *)gz_tilesolve_kernel<16, 1, false, 1>;
 }
 
+const void *pairs_kernel_lp16(int occ) {
+    return occ == 2 ? (const void *)gz_pairs_kernel<16, 1, 2> : (const void *)gz_pairs_kernel<16, 1, 1>;
+}
+
 }  // namespace gz4

@@ -791,13 +791,14 @@ bool index_fits(int rows, int cols, int m) {
 // host threads are serialised, calls on different devices run concurrently.
 struct DevicePool {
     std::mutex mu;
-    cudaStream_t streams[16] = {};
+    static constexpr int MAX_STREAMS = 128;   // concurrent pair solves (the hardware runs up to 128 kernels at once)
+    cudaStream_t streams[MAX_STREAMS] = {};
     bool have_streams = false;
     unsigned long long *pinned = nullptr;
     size_t pinned_n = 0;
     int streams_ready() {
         if (have_streams) return GZ_OK;
-        for (int k = 0; k < 16; ++k) CK(cudaStreamCreateWithFlags(&streams[k], cudaStreamNonBlocking));
+        for (int k = 0; k < MAX_STREAMS; ++k) CK(cudaStreamCreateWithFlags(&streams[k], cudaStreamNonBlocking));
         have_streams = true;
         return GZ_OK;
     }
@@ -958,10 +959,10 @@ struct Pending {
 // Enqueue one solve of the problem whose volume is already in w.vol (layout of
 // the chosen solver) on stream s, using 1/conc of the SMs.  Counters go to
 // h_ctr, labels to labels_out; collect with solve_finish after the stream.
-int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy *en, const gz_sched *sc,
-                 const int32_t *lo, const int32_t *hi, int32_t *labels_out, cudaStream_t s, int hcap, int conc,
-                 unsigned long long *h_ctr, Pending *pd, int max_width = -1, const BandPlan *bp = nullptr) {
-    Prob p;
+// Solver parameters of one problem (the schedule knobs and their tuning
+// overrides) and its state pointers into workspace w.
+void setup_prob(Prob &p, const Workspace &w, int rows, int cols, int m, const gz_energy *en, const gz_sched *sc,
+                const int32_t *lo, const int32_t *hi, int hcap) {
     memset(&p, 0, sizeof(p));
     p.Y = rows; p.G = cols; p.M = m; p.L = m - 1; p.P = rows * cols;
     p.inv_g = 1.0f / (float)cols;
@@ -980,25 +981,10 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
         p.watchdog_ns = (unsigned long long)(wd ? atof(wd) : def_ms) * 1000000ull;
     }
     p.trace = getenv("GZ_TRACE") ? atoi(getenv("GZ_TRACE")) : 0;
-    static unsigned long long *tbuf = nullptr;
-    if (p.trace > 1) {
-        if (!tbuf) CK(cudaMalloc((void **)&tbuf, 8192 * 8));
-        CK(cudaMemsetAsync(tbuf, 0, 8192 * 8, s));
-        p.tbuf = tbuf;
-    }
     p.lo = lo; p.hi = hi;
     p.vol = w.vol; p.cu = w.cu; p.ph = w.ph; p.pv = w.pv; p.dar = w.dar; p.dbr = w.dbr; p.dad = w.dad; p.dbd = w.dbd;
     p.e = w.e; p.ein = w.ein; p.h = w.h; p.h2 = w.h2; p.reach = w.reach; p.reach2 = w.reach2; p.labels = w.labels;
     p.ctr = w.ctr;
-    CK(cudaMemsetAsync(w.ctr, 0, gz::CTR_COUNT * 8, s));
-    CK(cudaEventCreate(&pd->e0));
-    CK(cudaEventCreate(&pd->e1));
-    pd->h_ctr = h_ctr;
-    pd->hard = p.hard;
-    pd->hcap = p.hcap;
-    CK(cudaEventRecord(pd->e0, s));
-    const bool win = lo != nullptr;
-    const int NW = words_for(m);
     const int which = choose_solver(m, sc);
     const bool v1 = which == 1;
     // Exact v4 solves stop a relabel early once it is max(24, m) levels deep and has
@@ -1039,6 +1025,33 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
         p.wl_dedupe = wd ? atoi(wd) : 1;   // measured: bench pulses -10%, C3q 1.76 -> 1.60 s
     }
     if (!v1 && p.bfs_cap < 0) p.bfs_cap = 0;            // exhaustive BFS every sweep
+    // one-CTA teams (batched pairs): the shared-memory tail mode takes over a sweep
+    // once its active groups fit the shared-memory worklist (GZ_TAIL_GROUPS)
+    p.tail_groups = getenv("GZ_TAIL_GROUPS") ? atoi(getenv("GZ_TAIL_GROUPS")) : 8;
+}
+
+int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy *en, const gz_sched *sc,
+                 const int32_t *lo, const int32_t *hi, int32_t *labels_out, cudaStream_t s, int hcap, int conc,
+                 unsigned long long *h_ctr, Pending *pd, int max_width = -1, const BandPlan *bp = nullptr) {
+    Prob p;
+    setup_prob(p, w, rows, cols, m, en, sc, lo, hi, hcap);
+    static unsigned long long *tbuf = nullptr;
+    if (p.trace > 1) {
+        if (!tbuf) CK(cudaMalloc((void **)&tbuf, 8192 * 8));
+        CK(cudaMemsetAsync(tbuf, 0, 8192 * 8, s));
+        p.tbuf = tbuf;
+    }
+    CK(cudaMemsetAsync(w.ctr, 0, gz::CTR_COUNT * 8, s));
+    CK(cudaEventCreate(&pd->e0));
+    CK(cudaEventCreate(&pd->e1));
+    pd->h_ctr = h_ctr;
+    pd->hard = p.hard;
+    pd->hcap = p.hcap;
+    CK(cudaEventRecord(pd->e0, s));
+    const bool win = lo != nullptr;
+    const int NW = words_for(m);
+    const int which = choose_solver(m, sc);
+    const bool v1 = which == 1;
     const void *kern = nullptr;
     const int LPn = lanes_for(m);
     // two CTAs per SM (64 registers, smaller BFS regions) for the m <= 16 instance
@@ -1129,27 +1142,15 @@ int solve_launch(const Workspace &w, int rows, int cols, int m, const gz_energy 
     return GZ_OK;
 }
 
-// Collect a solve once its stream has completed.
-int solve_finish(Pending &pd, gz_stats *st) {
-    if (pd.tbuf) {   // debug: dump the per-pulse trace
-        static unsigned long long h[8192];
-        CK(cudaMemcpy(h, pd.tbuf, sizeof(h), cudaMemcpyDeviceToHost));
-        for (int i = 0; i < 4096 && h[2 * i + 1]; ++i)
-            fprintf(stderr, "gz_pulse sweep %llu pulse %llu groups %llu dt_us %.2f\n", h[2 * i] >> 48,
-                    (h[2 * i] >> 32) & 0xffff, h[2 * i] & 0xffffffffull, h[2 * i + 1] * 1e-3);
-    }
-    float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, pd.e0, pd.e1));
-    cudaEventDestroy(pd.e0);
-    cudaEventDestroy(pd.e1);
-    const unsigned long long *h_ctr = pd.h_ctr;
+// Solver counters of one finished solve -> gz_stats (GZ_OK or its status).
+int stats_from_ctr(const unsigned long long *h_ctr, int hard, int hcap, float ms, int bfs_h, gz_stats *st) {
     if (h_ctr[CTR_ABORT]) return GZ_ERR_BANDS;
     if (h_ctr[CTR_STATUS]) return -(int)h_ctr[CTR_STATUS];
     if (st) {
         memset(st, 0, sizeof(*st));
         st->flow = (int64_t)h_ctr[CTR_FLOW];
-        if (pd.hard) {   // rescale uncuttable multiples to the reference's 2^56 (see gz_graph.cuh)
-            const int64_t k = st->flow / pd.hcap, f = st->flow % pd.hcap;
+        if (hard) {   // rescale uncuttable multiples to the reference's 2^56 (see gz_graph.cuh)
+            const int64_t k = st->flow / hcap, f = st->flow % hcap;
             st->flow = k * (int64_t)gz::UNCUTTABLE + f;
         }
         st->const_offset = (int64_t)h_ctr[CTR_OFFSET];
@@ -1174,11 +1175,27 @@ int solve_finish(Pending &pd, gz_stats *st) {
         st->bfs_passes = (int32_t)h_ctr[CTR_BFS_PASSES];
         st->reach_passes = (int32_t)h_ctr[CTR_REACH_PASSES];
         st->pulses = (int32_t)h_ctr[CTR_PULSES];
-        st->bfs_h = pd.bfs_h;
+        st->bfs_h = bfs_h;
         st->ms_total = ms;
         for (int q = 0; q < 6; ++q) st->ms_phase[q] = (float)(h_ctr[CTR_T0 + q] * 1e-6);
     }
     return GZ_OK;
+}
+
+// Collect a solve once its stream has completed.
+int solve_finish(Pending &pd, gz_stats *st) {
+    if (pd.tbuf) {   // debug: dump the per-pulse trace
+        static unsigned long long h[8192];
+        CK(cudaMemcpy(h, pd.tbuf, sizeof(h), cudaMemcpyDeviceToHost));
+        for (int i = 0; i < 4096 && h[2 * i + 1]; ++i)
+            fprintf(stderr, "gz_pulse sweep %llu pulse %llu groups %llu dt_us %.2f\n", h[2 * i] >> 48,
+                    (h[2 * i] >> 32) & 0xffff, h[2 * i] & 0xffffffffull, h[2 * i + 1] * 1e-3);
+    }
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, pd.e0, pd.e1));
+    cudaEventDestroy(pd.e0);
+    cudaEventDestroy(pd.e1);
+    return stats_from_ctr(pd.h_ctr, pd.hard, pd.hcap, ms, pd.bfs_h, st);
 }
 
 // Synchronous solve (one problem, all SMs).
@@ -1204,6 +1221,105 @@ int solve_planar(const Workspace &w, int rows, int cols, int m, const gz_energy 
     }
     CK(cudaStreamSynchronize(s));
     return solve_finish(pd, st);
+}
+
+// CTAs per team of the batched pair solves: 2 measured best (C1, 1184 pairs:
+// T = 1 / 2 / 4 -> 556 / 623 / 612 pairs/s; the round-1 one-launch-per-pair path
+// with 32 hardware queues: 529).  GZ_PAIR_TEAM overrides (0: the round-1 path).
+int pair_team() {
+    const char *tm = getenv("GZ_PAIR_TEAM");
+    return tm ? atoi(tm) : 2;
+}
+
+// Teams a batched pair solve runs side by side (one workspace slice each).
+int pair_teams(int m) {
+    const int T = pair_team();
+    if (lanes_for(m) != 16 || T <= 0) {
+        const char *cs = getenv("GZ_PAIR_CONC");
+        return cs ? atoi(cs) : 8;
+    }
+    int occ = 2;
+    if (const char *oc = getenv("GZ_OCC")) occ = atoi(oc) == 1 ? 1 : 2;
+    const void *kern = gz4::pairs_kernel_lp16(occ);
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gz4::smem_bytes(occ)) !=
+        cudaSuccess)
+        return 0;
+    int grid = 0;
+    if (coop_grid(kern, gz4::BLOCK, &grid, gz4::smem_bytes(occ))) return 0;
+    return grid / T;
+}
+
+// Batched teams (gz4::gz_pairs_kernel): the whole batch in ONE launch of
+// nteams x T CTAs, team k on workspace slice k, pairs handed out by a device
+// queue.  One-CTA teams (T = 1, the default) synchronise with CTA barriers
+// only and keep up to 2 x 148 pairs in flight.
+int solve_pairs_batched(const uint8_t *left, const uint8_t *right, int batch, int img_h, int img_w, int channels,
+                        const gz_cuboid *cb, const gz_energy *energy, const gz_sched *sched, int32_t *labels_out,
+                        gz_stats *stats_out, void *workspace, size_t workspace_bytes, cudaStream_t s, int T) {
+    const int rows = cb->y_extent, cols = cb->g_extent, m = cb->m, P = rows * cols;
+    const size_t one = ws_bytes(rows, cols, m);
+    int occ = 2;
+    if (const char *oc = getenv("GZ_OCC")) occ = atoi(oc) == 1 ? 1 : 2;
+    const void *kern = gz4::pairs_kernel_lp16(occ);
+    const size_t dyn = gz4::smem_bytes(occ);
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    int grid = 0;
+    int rc = coop_grid(kern, gz4::BLOCK, &grid, dyn);
+    if (rc) return rc;
+    int nteams = grid / T;
+    if ((size_t)nteams * one > workspace_bytes) nteams = (int)(workspace_bytes / one);
+    if (nteams > batch) nteams = batch;
+    if (nteams < 1) return GZ_ERR_WORKSPACE;
+    Workspace w = carve(workspace, rows, cols, m);
+    Prob p;
+    gz_sched sc = sched ? *sched : gz_sched{12, 0, 0, 0};
+    setup_prob(p, w, rows, cols, m, energy, &sc, nullptr, nullptr, 1 << 30);
+    p.tbuf = nullptr;
+    p.trace = 0;
+    p.labels = nullptr;   // per pair (PairBatch.labels_out)
+    if (!getenv("GZ_TAIL_GROUPS")) p.tail_groups = 8;
+    gz4::Geo geo = tile_geo(rows, cols, T, words_for(m), occ);
+    gz2::Bits2 bb = w.bits;
+    gz3::Arr3 a3{w.vol, w.cu, w.ph, w.pv, w.dar, w.dbr, w.dad, w.dbd, w.e, w.ein, w.h2, w.h, w.IN0, w.IN1};
+    gz4::PairBatch pb;
+    pb.left = left; pb.right = right; pb.img_w = img_w; pb.ch = channels;
+    pb.img_bytes = (size_t)img_h * img_w * channels;
+    pb.cb = *cb;
+    pb.batch = batch; pb.T = T;
+    pb.ws_stride = one;
+    pb.bits_bytes = w.bits_bytes;
+    pb.labels_out = labels_out;
+    unsigned long long *dbuf = nullptr;
+    const size_t sbytes = (size_t)batch * gz::CTR_COUNT * 8;
+    CK(cudaMallocAsync((void **)&dbuf, sbytes + 256, s));
+    pb.stats = dbuf;
+    pb.queue = (unsigned *)((uint8_t *)dbuf + sbytes);
+    CK(cudaMemsetAsync(pb.queue, 0, 16, s));
+    // team barrier words and counters of every slice start clear
+    for (int k = 0; k < nteams; ++k) {
+        Workspace wk = carve((uint8_t *)workspace + (size_t)k * one, rows, cols, m);
+        CK(cudaMemsetAsync(wk.ctr, 0, gz::CTR_COUNT * 8, s));
+    }
+    void *args[] = {&p, &bb, &a3, &geo, &pb};
+    grid = nteams * T;
+    CK(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(gz4::BLOCK), args, dyn, s));
+    DevicePool *pool = device_pool();
+    if (!pool) return GZ_ERR_CUDA;
+    std::lock_guard<std::mutex> lock(pool->mu);
+    if ((rc = pool->pinned_ready((size_t)batch * gz::CTR_COUNT))) return rc;
+    CK(cudaMemcpyAsync(pool->pinned, dbuf, sbytes, cudaMemcpyDeviceToHost, s));
+    cudaFreeAsync(dbuf, s);
+    CK(cudaStreamSynchronize(s));
+    for (int b = 0; b < batch && rc == GZ_OK; ++b) {
+        const unsigned long long *h = pool->pinned + (size_t)b * gz::CTR_COUNT;
+        rc = stats_from_ctr(h, energy->hard_inhibit ? 1 : 0, 1 << 30, (float)(h[CTR_NS] * 1e-6), geo.H,
+                            stats_out ? stats_out + b : nullptr);
+    }
+    if (rc) return rc;
+    if (stats_out)
+        for (int b = 0; b < batch; ++b)
+            if (stats_out[b].energy != stats_out[b].labeling_energy) return GZ_ERR_CONSISTENCY;
+    return GZ_OK;
 }
 
 }  // namespace
@@ -1328,11 +1444,20 @@ int gz_solve_pairs(const uint8_t *left, const uint8_t *right, int32_t batch, int
     cudaStream_t s = (cudaStream_t)stream;
     const size_t img = (size_t)img_h * img_w * channels;
     const int which = choose_solver(m, sched);
+    // 16-lane chains (m <= 16, BASELINE config 4): one launch of one-CTA teams
+    // (GZ_PAIR_TEAM = CTAs per team; 0 = one cooperative launch per pair on
+    // its own stream, the round-1 path)
+    {
+        const int T = pair_team();
+        if (which == 4 && lanes_for(m) == 16 && T > 0 && !(sched && (sched->flags & (GZ_SCHED_CAPPED | GZ_SCHED_INIT_ONLY))))
+            return solve_pairs_batched(left, right, batch, img_h, img_w, channels, cb, energy, sched, labels_out,
+                                       stats_out, workspace, workspace_bytes, (cudaStream_t)stream, T);
+    }
     // Concurrent solves: up to `conc` pairs run at once, each a cooperative launch
     // over 1/conc of the SMs on its own stream with its own workspace slice.
     int conc = 8;   // measured: 1 -> 250, 4 -> 366, 8 -> ~400 pairs/s (C1, 64 pairs per call)
     if (const char *cs = getenv("GZ_PAIR_CONC")) conc = atoi(cs);
-    if (conc > 16) conc = 16;
+    if (conc > DevicePool::MAX_STREAMS) conc = DevicePool::MAX_STREAMS;
     if ((size_t)conc * one > workspace_bytes) conc = (int)(workspace_bytes / one);
     if (conc > batch) conc = batch;
     if (which != 4 || conc < 1) conc = 1;
@@ -1486,6 +1611,14 @@ int gz_thin_skin(const int32_t *coarse_labels, int32_t crows, int32_t ccols, int
                                                                   radius, lo_out, hi_out);
     CK(cudaGetLastError());
     return GZ_OK;
+}
+
+size_t gz_pairs_workspace_bytes(int32_t rows, int32_t cols, int32_t m, int32_t batch) {
+    if (rows < 1 || cols < 1 || m < 2 || batch < 1 || !index_fits(rows, cols, m)) return 0;
+    int k = pair_teams(m);
+    if (k < 1) return 0;
+    if (k > batch) k = batch;
+    return (size_t)k * ws_bytes(rows, cols, m);
 }
 
 const char *gz_status_string(int status) {

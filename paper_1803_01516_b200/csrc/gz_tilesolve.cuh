@@ -83,6 +83,15 @@ struct Team {
         const unsigned w = __reduce_or_sync(FULL, flags);
         if ((threadIdx.x & 31) == 0 && w) atomicOr(&s_f3[k3], w);
         __syncthreads();
+        if (nb == 1) {
+            // a one-CTA team (batched pair solves): the CTA barrier is the team
+            // barrier.  Slot k3-1 was read by every thread before this barrier and
+            // is written again only at barrier k3+2, after thread 0 passed k3+1.
+            const unsigned f = s_f3[k3];
+            if (threadIdx.x == 0) s_f3[(k3 + 2) % 3] = 0u;
+            ++phase;
+            return (f & 1u) | ((f & 2u) << 15);
+        }
         if (threadIdx.x == 0) {
             const unsigned f = s_f3[k3];
             s_f3[(k3 + 1) % 3] = 0u;   // last read two barriers ago
@@ -281,8 +290,14 @@ __device__ unsigned bfs_round(const Prob &p, const Arr3 &a, const Bits2 &b, cons
 // ---------------------------------------------------------------------------
 // The solver.  LP = 16: two sites per warp group (m <= 16); LP = 32: one
 // (segment, site) per warp group, R segments per chain (m <= 32 R).
+// The whole solve of one problem by one team.  cta / ncta: this CTA's index
+// in its launch's share of the team and that share's size (a single launch:
+// blockIdx.x / gridDim.x; batched pair solves: the CTA's index in its team).
+// phase: the team barrier's running count (kept across the problems a
+// batched team solves, so its rotating barrier words stay consistent).
 template <int LP, int R, bool WIN, int OCC, int RW = 0>
-__global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 b, Arr3 a, Geo g, unsigned long long *bar) {
+__device__ __forceinline__ void tilesolve_body(Prob p, Bits2 b, Arr3 a, Geo g, unsigned long long *bar, const int cta,
+                                               const int ncta, int &phase) {
     // RW > 0: window-relative 16-lane groups over rows of 32 RW positions (gz_chain.cuh)
     constexpr int NW = RW ? RW : R, LPT = RW ? 32 * RW : LP * R;
     __shared__ unsigned s_f3[3], s_r3[3], s_qn[2];
@@ -290,15 +305,15 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
     __shared__ unsigned s_tn[2];  // tail-mode worklist lengths
     __shared__ unsigned s_wl[2];  // groups this CTA took from the pulse worklist (alternating)
     extern __shared__ uint32_t s_dyn[];
+    __syncthreads();   // (a batched team: every thread is done with the last problem's shared state)
     if (threadIdx.x < 3) { s_f3[threadIdx.x] = 0u; s_r3[threadIdx.x] = 0u; }
     if (threadIdx.x < 2) { s_qn[threadIdx.x] = 0u; s_wl[threadIdx.x] = 0u; }
     int qround = 0;
     __syncthreads();
-    int phase = 0;
     constexpr int RS = region_sites(NW, OCC);
     uint32_t *sF0 = s_dyn, *sF1 = s_dyn + NW * RS, *sM = s_dyn + 2 * NW * RS;
-    const bool resident = g.t1 - g.t0 <= (int)gridDim.x;   // one tile per CTA: masks stay in smem for the sweep
-    const Team tm{bar, p.ctr + CTR_ABORT, g.nb, g.rank0 + (int)blockIdx.x, g.sys,
+    const bool resident = g.t1 - g.t0 <= ncta;   // one tile per CTA: masks stay in smem for the sweep
+    const Team tm{bar, p.ctr + CTR_ABORT, g.nb, g.rank0 + cta, g.sys,
                   (unsigned long long)g.spin_ms * 1000000ull};
 #define TEAM_SYNC() (void)tm.sync_or(0u, phase, s_f3, s_r3)
 #define TEAM_OR(f) tm.sync_or((f), phase, s_f3, s_r3)
@@ -308,7 +323,7 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
     if (timer) t_prev = gz2::gtimer();
     if (timer) p.t_start_ns = t_prev;
 #define TICK(slot) do { if (timer) { unsigned long long t_ = gz2::gtimer(); t_acc[slot] += t_ - t_prev; t_prev = t_; } } while (0)
-#define FOR_TILES for (int tile = g.t0 + (int)blockIdx.x; tile < g.t1; tile += (int)gridDim.x)
+#define FOR_TILES for (int tile = g.t0 + cta; tile < g.t1; tile += ncta)
     long long flow = 0, offset = 0, presat = 0, pushes = 0, relabels = 0;
     volatile unsigned long long *vctr = p.ctr;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -320,11 +335,11 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
     // -> site pair gg0 + li (LP = 16), or (segment, site) word of the band's sites
     const int bsites = g.c1 - g.c0, bwords = NW * bsites;
     const int nloc = LP == 16 ? g.gg1 - g.gg0 : bwords;
-    const int gnw = (int)gridDim.x * nwarps, gwid = (int)blockIdx.x * nwarps + warp;
+    const int gnw = ncta * nwarps, gwid = cta * nwarps + warp;
     const int giter = (nloc + gnw - 1) / gnw;
     auto band_word = [&](int i) { const int s_ = i / bsites; return s_ * p.P + g.c0 + (i - s_ * bsites); };
     auto grp_of = [&](int li) { return LP == 16 ? g.gg0 + li : band_word(li); };
-    const int ttid = (int)blockIdx.x * blockDim.x + threadIdx.x, tstride = (int)gridDim.x * blockDim.x;
+    const int ttid = cta * (int)blockDim.x + (int)threadIdx.x, tstride = ncta * (int)blockDim.x;
     // tail mode: claim bitmap + two worklists in the (then idle) BFS shared memory
     const int tail_bw = (ngroups + 31) / 32;
     const int tail_cap = min(4096, ((int)(smem_bytes(OCC) / 4) - tail_bw) / 2);
@@ -454,6 +469,10 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
         // are idle during the BFS); a tile whose neighbourhood within H sites had no
         // frontier cannot gain nodes this round and only carries its words forward
         int32_t *tf_in = b.R1, *tf_out = b.R1 + g.ntiles;
+        // consecutive inactive rounds per tile: after two, both frontier/visited
+        // buffers already hold (no frontier, unchanged visited) and the tile's
+        // carry-forward copy is skipped (each tile is handled by one CTA)
+        int32_t *tl_idle = 3 * g.ntiles <= 2 * p.P ? b.R1 + 2 * g.ntiles : nullptr;
         const int rty = (g.H + g.TY - 1) / g.TY, rtx = (g.H + g.TX - 1) / g.TX;
         for (;;) {
             unsigned flags = 0;
@@ -469,10 +488,11 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
                         }
                 }
                 bool front = false;
+                const int idle = (d == 0 || !tl_idle) ? 0 : tl_idle[tile];
                 if (act) {
                     flags |= bfs_round<LPT, NW, WIN, OCC>(p, a, b, g, tb, Fin, Fout, Vin, Vout, d, sF0, sF1, sM,
                                                          d == 0 || !resident, front);
-                } else {
+                } else if (idle < 2) {
                     for (int r = tb.y0 + warp; r < tb.y1; r += nwarps)
                         for (int x = tb.x0 + lane; x < tb.x1; x += 32)
                             for (int w = 0; w < NW; ++w) {
@@ -481,7 +501,10 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
                                 Vout[q] = Vin[q];
                             }
                 }
-                if (threadIdx.x == 0) tf_out[tile] = front ? 1 : 0;
+                if (threadIdx.x == 0) {
+                    tf_out[tile] = front ? 1 : 0;
+                    if (tl_idle) tl_idle[tile] = act ? 0 : (idle < 2 ? idle + 1 : 2);
+                }
             }
             const unsigned gf = TEAM_OR(flags);
             if (!found && (gf & 2u)) d_found = d + g.H;
@@ -509,7 +532,7 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
         }
         if (wl_on) {
             for (int i = tm.rank * blockDim.x + threadIdx.x; i < 2 * wl_bw; i += tm.nb * blockDim.x) wl_bits[0][i] = 0u;
-            if (threadIdx.x == 0 && blockIdx.x == 0)
+            if (threadIdx.x == 0 && cta == 0)
                 for (int i = 0; i < 4; ++i) wl_n[i] = 0u;
         }
         TEAM_SYNC();
@@ -568,14 +591,25 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
                     const int *lst = wl_list[k4];
                     uint32_t *bits = wl_bits[pulse & 1];
                     unsigned mine = 0;
-                    for (int q = gwid; q < (int)n_cur; q += gnw) {
-                        const int gg = __ldcg(lst + q);
-                        unsigned old = 0u;
-                        if (lane == 0) old = gz_atomic_or(p, &bits[gg >> 5], 1u << (gg & 31));
-                        old = __shfl_sync(FULL, old, 0);
-                        if ((old >> (gg & 31)) & 1u) continue;   // already taken this pulse
-                        pulse_wl(LP == 16 ? 2 * gg : gg % p.P, LP == 16 ? 0 : gg / p.P);
-                        ++mine;
+                    // chunks of `per` consecutive entries per warp: the lanes load and
+                    // claim a whole chunk at once (one round trip), then the warp runs
+                    // the groups it won; chunks shrink to one entry when the list is
+                    // short next to the team's warps (load balance)
+                    const int per = min(32, max(1, (int)n_cur / gnw));
+                    for (int q0 = gwid * per; q0 < (int)n_cur; q0 += gnw * per) {
+                        const int qi = q0 + lane;
+                        const bool in = lane < per && qi < (int)n_cur;
+                        const int gg = in ? __ldcg(lst + qi) : 0;
+                        unsigned old = 1u << (gg & 31);
+                        if (in) old = gz_atomic_or(p, &bits[gg >> 5], 1u << (gg & 31));
+                        uint32_t won = __ballot_sync(FULL, in && !((old >> (gg & 31)) & 1u));
+                        while (won) {   // (a group listed twice in one chunk is won once)
+                            const int src = __ffs(won) - 1;
+                            won &= won - 1;
+                            const int g2 = __shfl_sync(FULL, gg, src);
+                            pulse_wl(LP == 16 ? 2 * g2 : g2 % p.P, LP == 16 ? 0 : g2 / p.P);
+                            ++mine;
+                        }
                     }
                     updates += mine;
                     if (lane == 0 && mine) atomicAdd(&s_wl[pulse & 1], mine);
@@ -592,7 +626,7 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
                         for (int q = ttid; q < (int)n_prev; q += tstride) bq[__ldcg(lq + q) >> 5] = 0u;
                     }
                 }
-                if (threadIdx.x == 0 && blockIdx.x == 0) wl_n[(k4 + 2) & 3] = 0u;   // refilled from pulse + 1 on
+                if (threadIdx.x == 0 && cta == 0) wl_n[(k4 + 2) & 3] = 0u;   // refilled from pulse + 1 on
             } else {
                 FOR_ACTIVE_GROUPS(b.A, IN_prev, updates, cta_groups, pulse_fn)
             }
@@ -612,8 +646,8 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
             parity ^= 1;
             ++pulses;
             if (idle) break;
-            if (tail_ok && p.async_l == 0 && !p.capped && sweeps >= p.tail_after && pulse + 1 < kp && (cnt >> 16) == 0u &&
-                (cnt & 0xffffu) <= TAIL_CTAS) {
+            if (tail_ok && p.async_l == 0 && !p.capped && sweeps >= p.tail_after && pulse + 1 < kp &&
+                (g.nb == 1 ? cta_groups <= p.tail_groups : ((cnt >> 16) == 0u && (cnt & 0xffffu) <= TAIL_CTAS))) {
                 // ---- tail mode: the few active groups go to CTA 0, which runs the rest of
                 // the sweep's pulses on a shared-memory worklist with CTA barriers only ----
                 const uint32_t *INn = parity ? a.IN0 : a.IN1;
@@ -753,6 +787,120 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 
         p.ctr[CTR_REACH_PASSES] = reach_passes;
         p.ctr[CTR_CONVERGED] = converged;
         p.ctr[CTR_PULSES] = pulses;
+    }
+}
+
+template <int LP, int R, bool WIN, int OCC, int RW = 0>
+__global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 b, Arr3 a, Geo g, unsigned long long *bar) {
+    int phase = 0;
+    tilesolve_body<LP, R, WIN, OCC, RW>(p, b, a, g, bar, (int)blockIdx.x, (int)gridDim.x, phase);
+}
+
+// ---------------------------------------------------------------------------
+// Batched pair solves (gz_solve_pairs, BASELINE config 4): ONE launch of
+// nteams x T CTAs; team k (CTAs kT .. kT+T-1) owns workspace slice k and takes
+// pairs from a global queue until the batch is done.  Per pair the team
+// computes the data term (energy.py:83-114 / k_sad) straight into its volume
+// plane, clears its bit planes and counters, runs the whole solve, and copies
+// its counters to the pair's stats row.  Small teams waste no time on
+// cross-SM barriers (T = 1: the CTA barrier is the team barrier) and keep many
+// pairs in flight; one launch avoids the per-stream concurrency limit of
+// separate cooperative launches (CUDA_DEVICE_MAX_CONNECTIONS).
+struct PairBatch {
+    const uint8_t *left, *right;   // batch x (img_h, img_w, ch) uint8
+    int img_w, ch;
+    size_t img_bytes;
+    gz_cuboid cb;
+    int batch, T;
+    size_t ws_stride;               // bytes between two teams' workspace slices
+    size_t bits_bytes;              // bytes of the bit planes to clear per pair
+    int32_t *labels_out;            // batch x P
+    unsigned long long *stats;      // batch x CTR_COUNT counters
+    unsigned *queue;                // next pair to hand out
+};
+
+template <typename T>
+__device__ __forceinline__ T *shifted(T *q, size_t off) { return q ? (T *)((uint8_t *)q + off) : q; }
+
+template <int LP, int R, int OCC>
+__global__ void __launch_bounds__(BLOCK, OCC) gz_pairs_kernel(Prob p0, Bits2 b0, Arr3 a0, Geo g, PairBatch pb) {
+    const int T = pb.T, team = (int)blockIdx.x / T, cta = (int)blockIdx.x % T;
+    const size_t off = (size_t)team * pb.ws_stride;
+    Prob p = p0;
+    p.vol = shifted(p.vol, off); p.cu = shifted(p.cu, off); p.ph = shifted(p.ph, off); p.pv = shifted(p.pv, off);
+    p.dar = shifted(p.dar, off); p.dbr = shifted(p.dbr, off); p.dad = shifted(p.dad, off); p.dbd = shifted(p.dbd, off);
+    p.e = shifted(p.e, off); p.ein = shifted(p.ein, off); p.h = shifted(p.h, off); p.h2 = shifted(p.h2, off);
+    p.reach = shifted(p.reach, off); p.reach2 = shifted(p.reach2, off); p.ctr = shifted(p.ctr, off);
+    Bits2 b = b0;
+    b.mask = shifted(b.mask, off); b.V = shifted(b.V, off); b.F0 = shifted(b.F0, off); b.F1 = shifted(b.F1, off);
+    b.A = shifted(b.A, off); b.IN = shifted(b.IN, off); b.EX = shifted(b.EX, off); b.RL = shifted(b.RL, off);
+    b.R0 = shifted(b.R0, off); b.R1 = shifted(b.R1, off);
+    Arr3 a = a0;
+    a.vol = shifted(a.vol, off); a.cu = shifted(a.cu, off); a.ph = shifted(a.ph, off); a.pv = shifted(a.pv, off);
+    a.dar = shifted(a.dar, off); a.dbr = shifted(a.dbr, off); a.dad = shifted(a.dad, off); a.dbd = shifted(a.dbd, off);
+    a.e = shifted(a.e, off); a.ein0 = shifted(a.ein0, off); a.ein1 = shifted(a.ein1, off); a.h = shifted(a.h, off);
+    a.IN0 = shifted(a.IN0, off); a.IN1 = shifted(a.IN1, off);
+    unsigned long long *bar = p.ctr + CTR_BAR0;
+    uint32_t *bits = b.mask;   // the bit planes are one contiguous run starting at the masks
+    const Team tm{bar, p.ctr + CTR_ABORT, T, cta, 0, 0ull};
+    __shared__ unsigned s_t3[3], s_u3[3];
+    __shared__ int s_pair;
+    if (threadIdx.x < 3) { s_t3[threadIdx.x] = 0u; s_u3[threadIdx.x] = 0u; }
+    __syncthreads();
+    int phase = 0;
+    const int P = p.P, ttid = cta * (int)blockDim.x + (int)threadIdx.x, tstride = T * (int)blockDim.x;
+    for (;;) {
+        // ---- next pair: CTA 0 of the team draws it, the team barrier publishes it ----
+        if (cta == 0 && threadIdx.x == 0) {
+            const int k = (int)atomicAdd(pb.queue, 1u);
+            if (T == 1) s_pair = k;
+            else *(volatile int *)&p.ctr[CTR_PAIR] = k;
+        }
+        (void)tm.sync_or(0u, phase, s_t3, s_u3);
+        const int pair = T == 1 ? s_pair : *(volatile int *)&p.ctr[CTR_PAIR];
+        if (pair >= pb.batch) break;
+        // ---- clear the team's bit planes and counters, data term into the volume plane ----
+        {
+            uint4 *z = reinterpret_cast<uint4 *>(bits);
+            const size_t n16 = pb.bits_bytes / 16;
+            for (size_t i = ttid; i < n16; i += tstride) z[i] = make_uint4(0u, 0u, 0u, 0u);
+            if (cta == 0 && threadIdx.x < CTR_COUNT && threadIdx.x != CTR_PAIR &&
+                (threadIdx.x < CTR_BAR0 || threadIdx.x > CTR_BAR0 + 2))
+                p.ctr[threadIdx.x] = 0ull;
+            const uint8_t *lp = pb.left + (size_t)pair * pb.img_bytes, *rp = pb.right + (size_t)pair * pb.img_bytes;
+            const gz_cuboid &cb = pb.cb;
+            for (int c = ttid; c < P; c += tstride) {
+                const int yi = c / cb.g_extent, gi = c - yi * cb.g_extent, gg = cb.g_min + gi;
+                const size_t row = (size_t)(cb.y_min + yi) * pb.img_w * pb.ch;
+                constexpr int LPT = LP * R;
+                for (int kk = 0; kk < LPT; ++kk) {
+                    int acc = 0;
+                    if (kk < cb.m) {   // geometry.py:325-335 site_columns, energy.py:96-113
+                        const int d = cb.d_min + kk;
+                        int xr = gg + d, xl = (cb.width - 1) + gg - d;
+                        xr = xr < 0 ? 0 : (xr > cb.width - 1 ? cb.width - 1 : xr);
+                        xl = xl < 0 ? 0 : (xl > cb.width - 1 ? cb.width - 1 : xl);
+                        for (int q = 0; q < pb.ch; ++q)
+                            acc += abs((int)lp[row + (size_t)xl * pb.ch + q] - (int)rp[row + (size_t)xr * pb.ch + q]);
+                    }
+                    a.vol[(size_t)c * LPT + kk] = acc;
+                }
+            }
+        }
+        __threadfence();
+        (void)tm.sync_or(0u, phase, s_t3, s_u3);
+        unsigned long long t0 = gz2::gtimer();
+        Prob q = p;
+        q.labels = pb.labels_out + (size_t)pair * P;
+        q.t_start_ns = t0;
+        tilesolve_body<LP, R, false, OCC, 0>(q, b, a, g, bar, cta, T, phase);
+        __threadfence();
+        (void)tm.sync_or(0u, phase, s_t3, s_u3);
+        if (cta == 0 && threadIdx.x < CTR_COUNT) {
+            unsigned long long v = ((volatile unsigned long long *)p.ctr)[threadIdx.x];
+            if (threadIdx.x == CTR_NS) v = gz2::gtimer() - t0;
+            pb.stats[(size_t)pair * CTR_COUNT + threadIdx.x] = v;
+        }
     }
 }
 

@@ -54,12 +54,12 @@ class PairSolver:
         self.sites = cuboid.y_extent * cuboid.g_extent
         self.ws_one = _lib.lib().gz_workspace_bytes(cuboid.y_extent, cuboid.g_extent, cuboid.num_labels)
         self._ws: Optional[torch.Tensor] = None
-        self.concurrency = int(os.environ.get("GZ_PAIR_CONC", "8"))
 
     def _workspace(self, extra: int = 0, batch: int = 1) -> torch.Tensor:
-        # room for up to `concurrency` pair solves in flight (gz_solve_pairs runs
-        # that many cooperative launches side by side, each on 1/k of the SMs)
-        need = self.ws_one * max(1, min(batch, self.concurrency)) + extra + 4096
+        # room for every pair solve the device keeps in flight (one workspace
+        # slice per team of the batched launch; gz_pairs_workspace_bytes)
+        y, g, m = self.cuboid.y_extent, self.cuboid.g_extent, self.cuboid.num_labels
+        need = max(self.ws_one, _lib.lib().gz_pairs_workspace_bytes(y, g, m, max(1, batch))) + extra + 4096
         if self._ws is None or self._ws.numel() < need:
             self._ws = torch.empty(need, dtype=torch.uint8, device=self.dev)
         return self._ws

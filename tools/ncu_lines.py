@@ -1,28 +1,38 @@
-"""Aggregate ncu warp-stall samples per CUDA source line.
-usage: ncu -i rep --page source --csv --print-source cuda,sass > x.csv; python tools/ncu_lines.py x.csv [top]"""
-import csv, collections, sys
-rows = list(csv.reader(open(sys.argv[1])))
-top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-agg = collections.Counter(); src = {}
-fname = None; hdr = None; line = None
-for r in rows:
+"""Per-source-line totals of an ncu report: instructions executed, L2 sectors
+(global), stall samples -- which source lines the kernel's work comes from.
+
+python tools/ncu_lines.py REP.ncu-rep [top]"""
+import collections, csv, io, subprocess, sys
+
+rep = sys.argv[1]
+top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+src = list(csv.reader(io.StringIO(subprocess.run(
+    ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"], capture_output=True, text=True).stdout)))
+cols = {}
+agg = {k: collections.Counter() for k in ("inst", "l2", "stall")}
+text, fname, line = {}, None, None
+for r in src:
     if not r:
         continue
-    if r[0] == 'File Path':
-        fname = r[1].split('/')[-1]; continue
-    if r[0] == 'Line No':
-        hdr = r; si = r.index('Warp Stall Sampling (All Samples)'); continue
-    if hdr is None or len(r) <= si:
+    if r[0] == "File Path":
+        fname = r[1].split("/")[-1]
+        continue
+    if r[0] == "Line No":
+        cols = {"inst": r.index("Instructions Executed"), "l2": r.index("L2 Theoretical Sectors Global"),
+                "stall": r.index("Warp Stall Sampling (All Samples)")}
+        continue
+    if not cols or len(r) <= max(cols.values()):
         continue
     if r[0]:
-        line = (fname, int(r[0])); src[line] = r[1][:100]
-    try:
-        v = float(r[si] or 0)
-    except ValueError:
-        continue
-    if line:
-        agg[line] += v
-tot = sum(agg.values())
-print("total samples", tot)
-for (f, l), v in agg.most_common(top):
-    print(f"{100*v/tot:5.1f}% {f}:{l}  {src.get((f,l),'')}")
+        line = (fname, int(r[0]))
+        text[line] = r[1].strip()[:80]
+        for k, i in cols.items():   # the cuda line rows carry the per-line totals
+            try:
+                agg[k][line] += float(r[i] or 0)
+            except ValueError:
+                pass
+for k in ("inst", "l2", "stall"):
+    tot = sum(agg[k].values()) or 1
+    print(f"\n== {k}: total {tot:.3e}")
+    for (f, l), v in agg[k].most_common(top):
+        print(f"{100 * v / tot:5.1f}%  {f}:{l}  {text.get((f, l), '')}")
