@@ -31,9 +31,11 @@
  *            commit   heights take effect, inboxes merge.
  *          A pulse in which no node had work ends the sweep.
  *   stop   converged when a BFS reaches no excess; capped after max_sweeps
- *          sweeps (the labeling is then read from the capped state).
- *   read   labels = lo + the prefix of each chain reachable in the residual
- *          network from the nodes holding excess (maxflow.py:267-320).
+ *          sweeps, after one more BFS run to exhaustion.
+ *   read   converged: labels = lo + the prefix of each chain reachable in the
+ *          residual network from the nodes holding excess (maxflow.py:267-320);
+ *          capped: every node that cannot reach the sink is on the source side
+ *          (labels = hi - the nodes the last BFS reached).
  *
  * Full-chain segments only: the caller ensures every chain is one warp segment
  * on the device (m <= 16, or windows <= 15 positions wide with m <= 64: the
@@ -225,9 +227,10 @@ int gzo_capped(const int32_t *vol, int rows, int cols, int m, int32_t penalty, i
         for (int c = 0; c < S->P; ++c)
             for (int t = lo[c] + 1; t <= hi[c]; ++t) ex[IX(c, t)] = S->e[IX(c, t)] > 0;
         int exhausted = 0;
-        const int found = bfs(S, H, bfs_min, &exhausted, ex, vis, NULL, q, nq);
+        const int last = sweeps >= max_sweeps;   /* the last BFS runs to exhaustion (read-out) */
+        const int found = bfs(S, H, last ? 0x7fffffff : bfs_min, &exhausted, ex, vis, NULL, q, nq);
         if (!found && exhausted) break;
-        if (sweeps >= max_sweeps) { converged = 0; break; }
+        if (last) { converged = 0; break; }
         for (int pulse = 0; pulse < K; ++pulse) {
             int work = 0;
             memset(rl, 0, (size_t)N);
@@ -320,7 +323,20 @@ int gzo_capped(const int32_t *vol, int rows, int cols, int m, int32_t penalty, i
         ++sweeps;
         if (sweeps > 1000000) break;
     }
-    /* ---- read-out: residual reach from the excess nodes (w_reach_init / bit_reach_iter) ---- */
+    /* ---- read-out ---- */
+    if (!converged) {
+        /* capped stop: the source side is every node that cannot reach the sink
+           (vis = the last, exhaustive BFS) -- a prefix of each chain */
+        for (int c = 0; c < S->P; ++c) {
+            int reach = 0;
+            for (int t = lo[c] + 1; t <= hi[c]; ++t) reach += vis[IX(c, t)];
+            labels[c] = hi[c] - reach;
+        }
+        report[0] = flow; report[1] = sweeps; report[2] = pulses; report[3] = converged;
+        free(buf); free(S->h); free(S->h2); free(ex); free(vis); free(rl); free(inb); free(q); free(nq);
+        return 0;
+    }
+    /* converged: residual reach from the excess nodes (w_reach_init / bit_reach_iter) */
     memset(vis, 0, (size_t)N);
     i64 qt = 0;
     for (int c = 0; c < S->P; ++c)

@@ -1003,11 +1003,12 @@ void setup_prob(Prob &p, const Workspace &w, int rows, int cols, int m, const gz
         if (const char *k = getenv("GZ_K")) p.K = atoi(k) > 0 ? atoi(k) : p.K;
         if (const char *bc = getenv("GZ_BFS_CAP")) p.bfs_cap = atoi(bc);
     }
-    // capped (level-2) solves: a reference sweep discharges every active node 12
-    // times (FIFO rounds, maxflow.py:183-250); a synchronous pulse moves excess one
-    // hop, so the GPU sweep runs 2m pulses (24-label ladder: converges inside the
-    // 8-sweep cap at b=3, tools/l2_quality.py)
-    if (p.capped && 2 * m > p.K) p.K = 2 * m;
+    // capped (level-2) solves run rounds_per_sweep pulses per sweep (the reference's
+    // parameter, maxflow.py:403-409; 12 by default) and read the labeling off the
+    // sink side of the capped preflow (gz_tilesolve.cuh), a speed / quality trade:
+    // 24-label ladder L2 b=3, 8 sweeps: K = 12 -> 4.9 ms, energy 791805 (reference
+    // L2b3 790883, L1b3 790627 in 5.0 ms); K = 24 -> 7.0 ms, 790728
+    // (tools/l2_speed.py, profiles/r2_runs/l2_speed.txt)
     if (p.capped)
         if (const char *ck = getenv("GZ_CAPPED_K")) p.K = atoi(ck) > 0 ? atoi(ck) : p.K;   // tuning override
     if (which == 4 && !p.capped) {   // tail sweeps: few active chains, pulses are cheap next to a global relabel

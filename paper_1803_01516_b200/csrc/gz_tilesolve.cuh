@@ -424,6 +424,7 @@ __device__ __forceinline__ void tilesolve_body(Prob p, Bits2 b, Arr3 a, Geo g, u
         return;
     }
     int sweeps = 0, levels_total = 0, pulses = 0, parity = 0;
+    const uint32_t *v_last = nullptr;   // capped stop: visited words of the final (exhaustive) BFS
     int converged = 1;
     bool err = false;
     int bfs_min = p.bfs_cap > 0 ? p.bfs_cap : (1 << 30);
@@ -465,6 +466,9 @@ __device__ __forceinline__ void tilesolve_body(Prob p, Bits2 b, Arr3 a, Geo g, u
         int d = 0, d_found = 0;
         bool found = false, exhausted = false;
         uint32_t *Fin = b.F0, *Fout = b.F1, *Vin = b.V, *Vout = b.RL;
+        // the capped solve's last sweep: its BFS runs to exhaustion, because the
+        // capped labeling is read from it (the nodes that cannot reach the sink)
+        const bool last = p.capped && sweeps >= p.max_sweeps;
         // per-tile "interior frontier nonempty" flags of the last round (reach arrays
         // are idle during the BFS); a tile whose neighbourhood within H sites had no
         // frontier cannot gain nodes this round and only carries its words forward
@@ -514,7 +518,7 @@ __device__ __forceinline__ void tilesolve_body(Prob p, Bits2 b, Arr3 a, Geo g, u
             int32_t *tt = tf_in; tf_in = tf_out; tf_out = tt;
             d += g.H;
             if (!(gf & 1u)) { exhausted = true; break; }
-            if (found && d >= bfs_min) break;
+            if (found && d >= bfs_min && !last) break;
             if (d > 4 * (p.P + p.M) + 4 * g.H) { if (threadIdx.x == 0 && tm.rank == 0) vctr[CTR_STATUS] = (unsigned long long)(-GZ_ERR_NOCONVERGE); err = true; break; }
         }
         levels_total += d;
@@ -524,7 +528,7 @@ __device__ __forceinline__ void tilesolve_body(Prob p, Bits2 b, Arr3 a, Geo g, u
         TICK(2);
         if (err) break;
         if (!found && exhausted) break;
-        if (p.capped && sweeps >= p.max_sweeps) { converged = 0; break; }
+        if (last) { converged = 0; v_last = Vin; break; }
         for (int i = ttid; i < bwords; i += tstride) {
             const int w = band_word(i);
             b.A[w] = Vin[w] & b.EX[w];
@@ -738,11 +742,18 @@ __device__ __forceinline__ void tilesolve_body(Prob p, Bits2 b, Arr3 a, Geo g, u
     FOR_TILES                                                                       \
     for (int r = TileBox(p, g, tile).y0 + warp, y1_ = TileBox(p, g, tile).y1; r < y1_; r += nwarps) \
         for (int x = TileBox(p, g, tile).x0 + lane, x1_ = TileBox(p, g, tile).x1; x < x1_; x += 32)
-    FOR_TILE_SITES gz3::w_reach_init<NW, WIN>(p, b, r * p.G + x);
+    // A capped stop reads the labeling off the last BFS instead: every node that
+    // cannot reach the sink in the residual network goes to the source side (a
+    // valid cut for any preflow; its cost is the sink inflow plus the excess
+    // still able to reach the sink, and it becomes a minimum cut as the capped
+    // preflow converges).  Reaching the sink is closed upward along a chain
+    // (uncuttable chain arcs down), so the source side is a prefix.
+    const bool capped_stop = v_last != nullptr;
+    if (!capped_stop) FOR_TILE_SITES gz3::w_reach_init<NW, WIN>(p, b, r * p.G + x);
     TEAM_SYNC();
     int reach_passes = 0;
     int32_t *Rin = b.R0, *Rout = b.R1;
-    for (;;) {
+    for (; !capped_stop;) {
         unsigned ch = 0;
         FOR_TILE_SITES ch |= gz2::bit_reach_iter<WIN, NW>(p, b, r * p.G + x, Rin, Rout) ? 1u : 0u;
         const bool any = TEAM_OR(ch) != 0;
@@ -756,7 +767,18 @@ __device__ __forceinline__ void tilesolve_body(Prob p, Bits2 b, Arr3 a, Geo g, u
     FOR_TILE_SITES {
         const int c = r * p.G + x;
         const int lo = WIN ? p.lo[c] : 0;
-        p.labels[c] = lo + Rin[c];
+        if (capped_stop) {
+            const int hi = WIN ? p.hi[c] : p.L;
+            BW<NW> v;
+            v.load(v_last, p.P, c);
+            v = v & BW<NW>::range(lo, hi);
+            int reach = 0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) reach += __popc(v.w[w]);
+            p.labels[c] = hi - reach;
+        } else {
+            p.labels[c] = lo + Rin[c];
+        }
         for (int w = 0; w < NW; ++w) stranded += __popc(b.EX[(size_t)w * p.P + c]);
     }
     TEAM_SYNC();

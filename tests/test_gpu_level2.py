@@ -3,7 +3,7 @@ deterministic schedule (oracle/gz_capped.c; the reference's
 sequential FIFO schedule, maxflow.py:198-249, cannot be replayed on a GPU, so
 the GPU schedule is restated and pinned bit for bit).  The restatement takes
 the device's BFS blocking depth (stats['bfs_h']); pulses per sweep and the
-BFS early-stop depth follow gz_solver.cu (max(rounds, 2m), max(24, m))."""
+BFS early-stop depth follow gz_solver.cu (rounds_per_sweep, max(24, m))."""
 
 import numpy as np
 import pytest
@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 
 def _restated(oracle, vol, p, lo, hi, max_sweeps, bfs_h, rounds=12):
     m = vol.shape[2]
-    return oracle.capped_schedule(vol, p.penalty, p.inhibit, lo, hi, K=max(rounds, 2 * m), max_sweeps=max_sweeps,
+    return oracle.capped_schedule(vol, p.penalty, p.inhibit, lo, hi, K=rounds, max_sweeps=max_sweeps,
                                   bfs_min=max(24, m), H=bfs_h)
 
 
