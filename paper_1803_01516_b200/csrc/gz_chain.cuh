@@ -212,15 +212,32 @@ struct TailQ {
 // All shuffles are executed by every lane (uniform control flow).
 template <int LP, int R, bool WIN, bool CG = false, int RW = 0>
 struct Arcs {
-    int r[A_COUNT], hv[A_COUNT];
+    int r[A_COUNT];
     unsigned snk;   // bit j: arc j leads into the sink (arcs into the source have r = 0)
+    unsigned adm;   // bit j: arc j admissible (residual > 0 and h(u) = h(target) + 1)
+    int best;       // relabel height: 1 + the lowest target height over residual arcs (HINF if none)
     // raw words (for write-back)
     int w_cu, w_ph, w_pv, w_dar, w_dbr, w_dad, w_dbd;   // own-stored at I
     int w_phL, w_pvU, w_darL, w_dbrL, w_dadU, w_dbdU;   // neighbour-stored at the same position
     int w_dbr_up, w_darL_up, w_dbd_up, w_dadU_up;       // same arrays at position t+1
     int h_u;
 
+    // target heights are folded into adm / best as soon as they are known (fewer
+    // live registers in w_pulse)
+    __device__ __forceinline__ void finish(const int (&hv)[A_COUNT]) {
+        adm = 0u;
+        best = HINF;
+#pragma unroll
+        for (int jj = 0; jj < A_COUNT; ++jj)
+            if (r[jj] > 0) {
+                const int c = hv[jj] + 1;
+                best = min(best, c);
+                if (h_u == c) adm |= 1u << jj;
+            }
+    }
+
     __device__ __forceinline__ void load(const Prob &p, const Arr3 &a, const Lane<LP, R, WIN, RW> &L) {
+        int hv[A_COUNT];
         const int I = L.I;
         const bool v = L.valid;
         w_cu = v ? ldx<CG>(a.cu + I) : 0;
@@ -279,6 +296,7 @@ struct Arcs {
             r[A_DL] = (L.has[1] && !bot) ? cap - w_dbrL : 0; hv[A_DL] = hn_below[1];
             r[A_DD] = (L.has[2] && !bot) ? cap - w_dad : 0; hv[A_DD] = hn_below[2];
             r[A_DU] = (L.has[3] && !bot) ? cap - w_dbdU : 0; hv[A_DU] = hn_below[3];
+            finish(hv);
             return;
         }
         snk = 0u;
@@ -298,6 +316,7 @@ struct Arcs {
         SETA(A_DD, L.has[2] ? cap - w_dad : 0, L.has[2] ? L.knb(2, t - 1) : K_SRC, hn_below[2]);
         SETA(A_DU, L.has[3] ? cap - w_dbdU : 0, L.has[3] ? L.knb(3, t - 1) : K_SRC, hn_below[3]);
 #undef SETA
+        finish(hv);
     }
 };
 
@@ -533,7 +552,7 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
     const int hu = A.h_u;
     const bool live = L.real && hu < HINF;
     // upward chain wave through admissible chain arcs
-    const bool adm_up = live && A.r[A_UP] > 0 && hu == A.hv[A_UP] + 1;
+    const bool adm_up = live && ((A.adm >> A_UP) & 1u);
     const int x_out = chain_wave<LP>(adm_up ? A.r[A_UP] : 0, adm_up ? max(e, 0) : 0, L.j);
     const int x_below = from_below<LP>(x_out);   // every lane shuffles (full mask)
     const int x_in = L.j > 0 ? x_below : 0;
@@ -554,49 +573,57 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
             }
         }
     }
-    // lateral and downward pushes of the remaining excess: admissible residuals
-    // in push order, then a short min/subtract allocation (independent of the
-    // arc bookkeeping, which follows as predicated selects)
-    int dd[A_COUNT];
+    // Lateral and downward pushes of the remaining excess along admissible arcs,
+    // in arc order.  Each push updates its arc pair's state at once (only this
+    // node pushes along that pair this pulse) and lands in the target's inbox;
+    // every inbox add and inbox-bit OR is issued before any result is used (one
+    // memory round trip for all of them), and the target groups that go on the
+    // worklist are appended after the write-back with one warp-aggregated atomic
+    // (TailQ::reserve_warp).  Asynchronous pulses apply pair-state deltas
+    // atomically (concurrent opposite pushes stay within capacity because each is
+    // bounded by its own stale-low read).
+    uint32_t lmask = 0u;   // bit jj: lateral push along arc jj into a real node
+    uint32_t dup = 0u;     // bit jj: its inbox word was already set this pulse
+    int dn = 0;            // chain-down push
     {
         int rem = (live && e > 0) ? e : 0;
+        const int iL = L.nidx(1), iU = L.nidx(3);
+#define GZ_PAIR(arr, idx, word, delta) do { if (ASYNC) atomicAdd(&a.arr[idx], (delta)); else a.arr[idx] = (word) + (delta); } while (0)
 #pragma unroll
         for (int jj = A_SR; jj <= A_DN; ++jj) {
-            const bool adm = A.r[jj] > 0 && hu == A.hv[jj] + 1;
-            const int d = adm ? min(rem, A.r[jj]) : 0;
-            dd[jj] = d;
+            const int d = ((A.adm >> jj) & 1u) ? min(rem, A.r[jj]) : 0;
             rem -= d;
+            if (d <= 0) continue;
+            pushed = true;
+            ++pushes;
+            switch (jj) {
+            case A_SR: GZ_PAIR(ph, I, A.w_ph, -d); break;
+            case A_SD: GZ_PAIR(pv, I, A.w_pv, -d); break;
+            case A_DR: GZ_PAIR(dar, I, A.w_dar, d); break;
+            case A_DD: GZ_PAIR(dad, I, A.w_dad, d); break;
+            case A_SL: GZ_PAIR(ph, iL, A.w_phL, d); break;
+            case A_DL: GZ_PAIR(dbr, iL, A.w_dbrL, d); break;
+            case A_SU: GZ_PAIR(pv, iU, A.w_pvU, d); break;
+            case A_DU: GZ_PAIR(dbd, iU, A.w_dbdU, d); break;
+            case A_UR: GZ_PAIR(dbr, I + 1, A.w_dbr_up, -d); break;
+            case A_UD: GZ_PAIR(dbd, I + 1, A.w_dbd_up, -d); break;
+            case A_UL: GZ_PAIR(dar, iL + 1, A.w_darL_up, -d); break;
+            case A_UU: GZ_PAIR(dad, iU + 1, A.w_dadU_up, -d); break;
+            default: break;
+            }
+            if (jj == A_DN) { dn = d; continue; }
+            if ((A.snk >> jj) & 1u) { flow += d; continue; }
+            int site, pos;
+            lateral_target(L, jj, site, pos);
+            gz_atomic_add(p, &ein_cur[site * LPT + pos - 1], d);
+            uint32_t *inw = &IN_cur[((pos - 1) >> 5) * P + site];
+            const uint32_t bit = 1u << ((pos - 1) & 31);
+            if (tq) dup |= (gz_atomic_or(p, inw, bit) != 0u ? 1u : 0u) << jj;
+            else gz_atomic_or(p, inw, bit);
+            lmask |= 1u << jj;
         }
+#undef GZ_PAIR
         if (live && e > 0) e = rem;
-    }
-    const int ph_d = -dd[A_SR], pv_d = -dd[A_SD], dar_d = dd[A_DR], dad_d = dd[A_DD];
-    const int phL_d = dd[A_SL], pvU_d = dd[A_SU], dbrL_d = dd[A_DL], dbdU_d = dd[A_DU];
-    const int dbr_up_d = -dd[A_UR], darL_up_d = -dd[A_UL], dbd_up_d = -dd[A_UD], dadU_up_d = -dd[A_UU];
-    const int dn = dd[A_DN];
-    // Every inbox add and inbox-bit OR of this node is issued before any result
-    // is used (one memory round trip for all of them); the target groups that
-    // go on the worklist are appended after the write-back with one
-    // warp-aggregated atomic (TailQ::reserve_warp) instead of one returning
-    // atomic per push.
-    uint32_t lmask = 0u;            // bit jj: lateral push along arc jj into a real node
-    uint32_t olds[A_COUNT];
-#pragma unroll
-    for (int jj = A_SR; jj <= A_DN; ++jj) {
-        const int d = dd[jj];
-        olds[jj] = 0u;
-        if (d <= 0) continue;
-        pushed = true;
-        ++pushes;
-        if (jj == A_DN) continue;
-        if ((A.snk >> jj) & 1u) { flow += d; continue; }
-        int site, pos;
-        lateral_target(L, jj, site, pos);
-        gz_atomic_add(p, &ein_cur[site * LPT + pos - 1], d);
-        uint32_t *inw = &IN_cur[((pos - 1) >> 5) * P + site];
-        const uint32_t bit = 1u << ((pos - 1) & 31);
-        if (tq) olds[jj] = gz_atomic_or(p, inw, bit);
-        else gz_atomic_or(p, inw, bit);
-        lmask |= 1u << jj;
     }
     // chain-down pushes arrive at lane j-1 (adds to its excess and to its chain-up
     // residual); out of a segment's first lane they cross into the segment below
@@ -615,49 +642,17 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
     // relabel a live node that could not push (deterministic mode: a later phase)
     int hnew = hu;
     if (!DETPUSH && live && !pushed && e > 0) {
-        int best = HINF;
-#pragma unroll
-        for (int jj = 0; jj < A_COUNT; ++jj)
-            if (A.r[jj] > 0) best = min(best, A.hv[jj] + 1);
-        hnew = best;
+        hnew = A.best;
         ++relabels;
     }
-    // write back
-    if (ASYNC && L.real) {
-        // pair states (and the chain residual, which a segment above can change)
-        // as atomic deltas: concurrent opposite pushes on one arc pair stay within
-        // its capacity because each push is bounded by its own (stale-low) read
+    // write back the node's own excess, chain residual and height
+    if (L.real) {
         a.e[I] = e;
-        if (cu_new != A.w_cu) atomicAdd(&a.cu[I], cu_new - A.w_cu);
+        if (cu_new != A.w_cu) {
+            if (ASYNC) atomicAdd(&a.cu[I], cu_new - A.w_cu);   // (a segment above can change it too)
+            else a.cu[I] = cu_new;
+        }
         if (hnew != hu) a.h[I] = hnew;
-        if (ph_d) atomicAdd(&a.ph[I], ph_d);
-        if (pv_d) atomicAdd(&a.pv[I], pv_d);
-        if (dar_d) atomicAdd(&a.dar[I], dar_d);
-        if (dad_d) atomicAdd(&a.dad[I], dad_d);
-        if (phL_d) atomicAdd(&a.ph[L.nidx(1)], phL_d);
-        if (dbrL_d) atomicAdd(&a.dbr[L.nidx(1)], dbrL_d);
-        if (pvU_d) atomicAdd(&a.pv[L.nidx(3)], pvU_d);
-        if (dbdU_d) atomicAdd(&a.dbd[L.nidx(3)], dbdU_d);
-        if (dbr_up_d) atomicAdd(&a.dbr[I + 1], dbr_up_d);
-        if (dbd_up_d) atomicAdd(&a.dbd[I + 1], dbd_up_d);
-        if (darL_up_d) atomicAdd(&a.dar[L.nidx(1) + 1], darL_up_d);
-        if (dadU_up_d) atomicAdd(&a.dad[L.nidx(3) + 1], dadU_up_d);
-    } else if (L.real) {
-        a.e[I] = e;
-        if (cu_new != A.w_cu) a.cu[I] = cu_new;
-        if (hnew != hu) a.h[I] = hnew;
-        if (ph_d) a.ph[I] = A.w_ph + ph_d;
-        if (pv_d) a.pv[I] = A.w_pv + pv_d;
-        if (dar_d) a.dar[I] = A.w_dar + dar_d;
-        if (dad_d) a.dad[I] = A.w_dad + dad_d;
-        if (phL_d) a.ph[L.nidx(1)] = A.w_phL + phL_d;
-        if (dbrL_d) a.dbr[L.nidx(1)] = A.w_dbrL + dbrL_d;
-        if (pvU_d) a.pv[L.nidx(3)] = A.w_pvU + pvU_d;
-        if (dbdU_d) a.dbd[L.nidx(3)] = A.w_dbdU + dbdU_d;
-        if (dbr_up_d) a.dbr[I + 1] = A.w_dbr_up + dbr_up_d;
-        if (dbd_up_d) a.dbd[I + 1] = A.w_dbd_up + dbd_up_d;
-        if (darL_up_d) a.dar[L.nidx(1) + 1] = A.w_darL_up + darL_up_d;
-        if (dadU_up_d) a.dad[L.nidx(3) + 1] = A.w_dadU_up + dadU_up_d;
     }
     const uint32_t newA = seg_ballot<LP>(L.real && e > 0 && hnew < HINF && (!DETPUSH || pushed));
     uint32_t rl = 0u;
@@ -680,7 +675,7 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
         uint32_t want = 0u;
 #pragma unroll
         for (int jj = A_SR; jj < A_DN; ++jj)
-            if (((lmask >> jj) & 1u) && !(olds[jj] && tq->dedupe)) want |= 1u << jj;
+            if (((lmask >> jj) & 1u) && !(((dup >> jj) & 1u) && tq->dedupe)) want |= 1u << jj;
         const bool self = __any_sync(FULL, newA != 0u) && (threadIdx.x & 31) == 0;
         auto gid = [&](int jj) {
             int site, pos;
@@ -726,11 +721,7 @@ __device__ void w_relabel(const Prob &p, const Arr3 &a, const Bits2 &b, int c_ba
     Arcs<LP, R, WIN, false, RW> A;
     A.load(p, a, L);
     if (L.valid && ((rl >> L.bbit()) & 1u)) {
-        int best = HINF;
-#pragma unroll
-        for (int jj = 0; jj < A_COUNT; ++jj)
-            if (A.r[jj] > 0) best = min(best, A.hv[jj] + 1);
-        h2[L.I] = best;
+        h2[L.I] = A.best;
         ++relabels;
     }
 }
