@@ -618,8 +618,8 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
             gz_atomic_add(p, &ein_cur[site * LPT + pos - 1], d);
             uint32_t *inw = &IN_cur[((pos - 1) >> 5) * P + site];
             const uint32_t bit = 1u << ((pos - 1) & 31);
-            if (tq) dup |= (gz_atomic_or(p, inw, bit) != 0u ? 1u : 0u) << jj;
-            else gz_atomic_or(p, inw, bit);
+            if (tq && tq->dedupe) dup |= (gz_atomic_or(p, inw, bit) != 0u ? 1u : 0u) << jj;
+            else gz_atomic_or(p, inw, bit);   // (result unused: a fire-and-forget reduction)
             lmask |= 1u << jj;
         }
 #undef GZ_PAIR

@@ -16,7 +16,7 @@
 //    site groups are interleaved over all warps of the team, and each warp
 //    checks its groups' active/inbox words with one load per lane + a ballot,
 //    visiting only the chains that have work.
-//  * extraction (maxflow.py:267-320): prefix-closure rounds (gz_bitsolve.cuh).
+//  * extraction (maxflow.py:267-320): prefix-closure rounds (gz_bits.cuh).
 //  * chains longer than 32 positions are split into R segments of 32 lanes
 //    (gz_chain.cuh); bit words and the BFS are NW = R words per site.
 //
@@ -478,19 +478,33 @@ __device__ __forceinline__ void tilesolve_body(Prob p, Bits2 b, Arr3 a, Geo g, u
         // carry-forward copy is skipped (each tile is handled by one CTA)
         int32_t *tl_idle = 3 * g.ntiles <= 2 * p.P ? b.R1 + 2 * g.ntiles : nullptr;
         const int rty = (g.H + g.TY - 1) / g.TY, rtx = (g.H + g.TX - 1) / g.TX;
+        // a tile is active in a round if a tile within H sites had frontier in the
+        // last one; the flags of all of this CTA's tiles are gathered at the start of
+        // the round by its threads in parallel (independent loads: one round trip
+        // instead of up to 9 dependent ones per tile), into s_q (idle during BFS)
+        auto tile_act = [&](int tile) {
+            const int ty = tile / g.nx, tx = tile - ty * g.nx;
+            bool a_ = false;
+            for (int dy = -rty; dy <= rty; ++dy)
+                for (int dx = -rtx; dx <= rtx; ++dx) {
+                    const int yy = ty + dy, xx = tx + dx;
+                    if (yy >= 0 && yy < g.ny && xx >= 0 && xx < g.nx) a_ |= __ldcg(tf_in + yy * g.nx + xx) != 0;
+                }
+            return a_;
+        };
         for (;;) {
             unsigned flags = 0;
+            if (d > 0) {
+                for (int k = threadIdx.x, tile = g.t0 + cta + k * ncta; k < BLOCK && tile < g.t1;
+                     k += blockDim.x, tile += (int)blockDim.x * ncta)
+                    s_q[k] = tile_act(tile) ? 1 : 0;
+                __syncthreads();
+            }
+            int tk = 0;
             FOR_TILES {
                 const TileBox tb(p, g, tile);
-                bool act = d == 0;
-                if (!act) {
-                    const int ty = tile / g.nx, tx = tile - ty * g.nx;
-                    for (int dy = -rty; dy <= rty && !act; ++dy)
-                        for (int dx = -rtx; dx <= rtx && !act; ++dx) {
-                            const int yy = ty + dy, xx = tx + dx;
-                            if (yy >= 0 && yy < g.ny && xx >= 0 && xx < g.nx) act = __ldcg(tf_in + yy * g.nx + xx) != 0;
-                        }
-                }
+                const bool act = d == 0 || (tk < BLOCK ? s_q[tk] != 0 : tile_act(tile));
+                ++tk;
                 bool front = false;
                 const int idle = (d == 0 || !tl_idle) ? 0 : tl_idle[tile];
                 if (act) {

@@ -8,8 +8,6 @@ reference-facing end-to-end call (host buffers in, host labels out).
 
 from __future__ import annotations
 
-import os
-
 import ctypes as C
 from typing import Optional
 

@@ -4,7 +4,7 @@ the knobs are environment variables read per call (gz_solver.cu setup_prob).
 python tools/knob_sweep.py PAIRS 'NAME=V,NAME2=V2' 'NAME=V' ..."""
 import os, sys, time
 sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "/root/repo"))
-os.environ.setdefault("GZ_PAIR_CONC", "296")
+
 import numpy as np, torch
 import paper_1803_01516_b200 as gz
 n = int(sys.argv[1])
