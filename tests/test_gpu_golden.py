@@ -103,3 +103,37 @@ def test_level2_deterministic_and_near_level1(gz):
     assert np.array_equal(a.labeling, b.labeling) and a.energy == b.energy
     lad = G["ladder24"]
     assert lad["l1b3"]["energy"] <= a.energy <= lad["l2b3"]["energy"] * 1.0025
+
+
+@pytest.mark.parametrize("team", ["1", "2", "4", "0"])
+def test_pair_batches_every_team_size(gz, monkeypatch, team):
+    """gz_solve_pairs' batched launch with teams of 1 / 2 / 4 CTAs, and the
+    round-1 one-launch-per-pair path (GZ_PAIR_TEAM=0): the reference's C1
+    fixtures bit for bit, with more pairs than teams on a small team count."""
+    monkeypatch.setenv("GZ_PAIR_TEAM", team)
+    cub = gz.cuboid_from_disparity_range(384, 288, 10, 28, num_labels=16)
+    scenes = [gz.make_scene(s) for s in range(8)]
+    left = torch.from_numpy(np.stack([s.left for s in scenes]))
+    right = torch.from_numpy(np.stack([s.right for s in scenes]))
+    solver = gz.PairSolver(cub, gz.EnergyParams(14, 1023), 288, 384, 3)
+    labels, stats = solver.solve(left, right)
+    for seed, want in enumerate(G["c1_exact"]):
+        assert stats[seed]["flow"] == want["flow"], (team, seed)
+        assert sha(labels[seed].cpu().numpy()) == want["labeling"], (team, seed)
+
+
+@pytest.mark.parametrize("hard", [False, True])
+def test_pair_batches_small_scenes_match_oracle(gz, oracle, hard):
+    """Batched pairs on small scenes (m = 6, grey and colour) and hard inhibit,
+    against the oracle's sad_volume + solve_exact per pair."""
+    cub = gz.cuboid_from_disparity_range(64, 32, 2, 9, num_labels=6)
+    p = gz.EnergyParams(5, 40, hard)
+    scenes = [gz.make_scene(s, 64, 32, 2, 9) for s in range(12)]
+    left = torch.from_numpy(np.stack([s.left for s in scenes]))
+    right = torch.from_numpy(np.stack([s.right for s in scenes]))
+    labels, stats = gz.PairSolver(cub, p, 32, 64, 3).solve(left, right)
+    for i, s in enumerate(scenes):
+        vol = oracle.sad_volume(s.left, s.right, cub.g_min, cub.g_extent, cub.y_min, cub.y_extent, cub.d_min, 6)
+        want = oracle.solve_exact(vol, 5, 40, hard)
+        assert stats[i]["flow"] == want["flow"] and stats[i]["energy"] == want["energy"], (i, hard)
+        assert np.array_equal(labels[i].cpu().numpy(), want["labeling"]), (i, hard)
