@@ -509,6 +509,9 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
     L.init(p, c_base, nsites, seg);
     const int I = L.I, P = p.P;
     constexpr int LPT = Lane<LP, R, WIN, RW>::LPT;
+    // worklist fields read once (the queue lives in local / shared memory and the
+    // list stores below could alias it, so the compiler would reload them per use)
+    const bool dedupe = tq && tq->dedupe;
     // synchronous pulses double-buffer the inbox by parity; asynchronous ones use
     // one buffer consumed atomically
     uint32_t *IN_prev = (ASYNC || parity) ? a.IN0 : a.IN1;
@@ -618,7 +621,7 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
             gz_atomic_add(p, &ein_cur[site * LPT + pos - 1], d);
             uint32_t *inw = &IN_cur[((pos - 1) >> 5) * P + site];
             const uint32_t bit = 1u << ((pos - 1) & 31);
-            if (tq && tq->dedupe) dup |= (gz_atomic_or(p, inw, bit) != 0u ? 1u : 0u) << jj;
+            if (dedupe) dup |= (gz_atomic_or(p, inw, bit) != 0u ? 1u : 0u) << jj;
             else gz_atomic_or(p, inw, bit);   // (result unused: a fire-and-forget reduction)
             lmask |= 1u << jj;
         }
@@ -675,7 +678,7 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
         uint32_t want = 0u;
 #pragma unroll
         for (int jj = A_SR; jj < A_DN; ++jj)
-            if (((lmask >> jj) & 1u) && !(((dup >> jj) & 1u) && tq->dedupe)) want |= 1u << jj;
+            if (((lmask >> jj) & 1u) && !(((dup >> jj) & 1u) && dedupe)) want |= 1u << jj;
         const bool self = __any_sync(FULL, newA != 0u) && (threadIdx.x & 31) == 0;
         auto gid = [&](int jj) {
             int site, pos;
@@ -683,11 +686,28 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
             return LP == 16 ? site >> 1 : ((pos - 1) / LP) * P + site;
         };
         if (tq->aggregated()) {
-            int k = tq->reserve_warp(__popc(want) + (self ? 1 : 0));
+            int *const lst = tq->rt ? tq->rt->list : tq->q;
+            unsigned *const cnt = tq->rt ? tq->rt->cnt : tq->n;
+            const int cap = tq->rt ? tq->rt->nw * tq->rt->P : tq->cap;
+            // warp-aggregated append: lane prefix of the entry counts, ONE atomic
+            const int lane = threadIdx.x & 31, mine = __popc(want) + (self ? 1 : 0);
+            int incl = mine;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(FULL, incl, o);
+                if (lane >= o) incl += v;
+            }
+            const int total = __shfl_sync(FULL, incl, 31);
+            unsigned base = 0u;
+            if (lane == 0 && total) base = atomicAdd(cnt, (unsigned)total);
+            int k = (int)__shfl_sync(FULL, base, 0) + incl - mine;
 #pragma unroll
             for (int jj = A_SR; jj < A_DN; ++jj)
-                if ((want >> jj) & 1u) tq->store(k++, gid(jj));
-            if (self) tq->store(k, LP == 16 ? c_base >> 1 : L.wi);
+                if ((want >> jj) & 1u) {
+                    if (k < cap) lst[k] = gid(jj);
+                    ++k;
+                }
+            if (self && k < cap) lst[k] = LP == 16 ? c_base >> 1 : L.wi;
         } else {
 #pragma unroll
             for (int jj = A_SR; jj < A_DN; ++jj)
