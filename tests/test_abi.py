@@ -114,3 +114,35 @@ def test_stats_struct_matches_header():
     body = body[: body.index("} gz_stats;")]
     names = re.findall(r"\b([a-z_][a-z_0-9]*)(?:\[\d+\])?\s*[,;]", re.sub(r"/\*.*?\*/", "", body, flags=re.S))
     assert names == [f[0] for f in _lib.Stats._fields_]
+
+
+def test_explicit_network_entry_points_reject_bad_arguments():
+    """The explicit-network C ABI (gz_csr.cuh) validates before any device work."""
+    import ctypes as C
+    L = _lib.lib()
+    p = C.c_void_p(16)
+    st = _lib.CsrStats()
+    info = (C.c_int64 * 4)()
+    en = _lib.Energy(14, 1023, 0)
+    # export: missing volume (capacity mode), bad windows pairing, m > 256
+    assert L.gz_export_arcs(None, 4, 5, 4, C.byref(en), None, None, 0, None, None, None, None, 0, info, p, 1 << 30,
+                            None) == _lib.GZ_ERR_ARG
+    assert L.gz_export_arcs(p, 4, 5, 4, C.byref(en), p, None, 0, None, None, None, None, 0, info, p, 1 << 30,
+                            None) == _lib.GZ_ERR_ARG
+    assert L.gz_export_arcs(p, 4, 5, 300, C.byref(en), None, None, 0, None, None, None, None, 0, info, p, 1 << 30,
+                            None) == _lib.GZ_ERR_ARG
+    assert L.gz_export_state(None, 4, 5, 4, 0, p, None) == _lib.GZ_ERR_ARG
+    assert L.gz_export_state(p, 4, 5, 4, 99, p, None) == _lib.GZ_ERR_ARG
+    # CSR max-flow: source == sink, out-of-range terminals, zero rounds, small workspace
+    args = lambda n, s, t, rounds, ws: L.gz_maxflow_csr(n, s, t, p, p, p, p, p, rounds, -1, None, None,  # noqa: E731
+                                                         C.byref(st), p, ws, None)
+    assert args(10, 3, 3, 12, 1 << 30) == _lib.GZ_ERR_ARG
+    assert args(10, 0, 10, 12, 1 << 30) == _lib.GZ_ERR_ARG
+    assert args(10, 0, 9, 0, 1 << 30) == _lib.GZ_ERR_ARG
+    assert args(10, 0, 9, 12, 16) == _lib.GZ_ERR_WORKSPACE
+    assert L.gz_csr_workspace_bytes(1) == 0 and L.gz_csr_workspace_bytes(1000) > 8000
+    assert L.gz_source_side_csr(10, 10, p, p, p, p, None) == _lib.GZ_ERR_ARG
+    assert L.gz_chain_presaturate_csr(None, p, p, p, 4, p, None) == _lib.GZ_ERR_ARG
+    assert L.gz_conservation_violations_csr(p, p, None, 4, 0, 3, p, None) == _lib.GZ_ERR_ARG
+    # batched-pair workspace: invalid shapes size to 0 (no device query needed)
+    assert L.gz_pairs_workspace_bytes(0, 5, 16, 8) == 0 and L.gz_pairs_workspace_bytes(4, 5, 1, 8) == 0
