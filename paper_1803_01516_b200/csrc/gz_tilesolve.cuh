@@ -295,8 +295,13 @@ __device__ unsigned bfs_round(const Prob &p, const Arr3 &a, const Bits2 &b, cons
 // blockIdx.x / gridDim.x; batched pair solves: the CTA's index in its team).
 // phase: the team barrier's running count (kept across the problems a
 // batched team solves, so its rotating barrier words stay consistent).
-template <int LP, int R, bool WIN, int OCC, int RW = 0>
-__device__ __forceinline__ void tilesolve_body(Prob p, Bits2 b, Arr3 a, Geo g, unsigned long long *bar, const int cta,
+// PP / BB / AA: how the descriptors are held -- by reference to the kernel's
+// __grid_constant__ parameters (one launch: read in place from the constant
+// bank), or by value (batched teams: per-team shifted copies the compiler can
+// keep in registers).
+template <int LP, int R, bool WIN, int OCC, int RW = 0, class PP = const Prob &, class BB = const Bits2 &,
+          class AA = const Arr3 &>
+__device__ __forceinline__ void tilesolve_body(PP p, BB b, AA a, const Geo &g, unsigned long long *bar, const int cta,
                                                const int ncta, int &phase) {
     // RW > 0: window-relative 16-lane groups over rows of 32 RW positions (gz_chain.cuh)
     constexpr int NW = RW ? RW : R, LPT = RW ? 32 * RW : LP * R;
@@ -321,7 +326,7 @@ __device__ __forceinline__ void tilesolve_body(Prob p, Bits2 b, Arr3 a, Geo g, u
     unsigned long long t_prev = 0, t_acc[6] = {0, 0, 0, 0, 0, 0};
     const bool timer = tm.rank == 0 && threadIdx.x == 0;
     if (timer) t_prev = gz2::gtimer();
-    if (timer) p.t_start_ns = t_prev;
+    const unsigned long long t_start = t_prev;   // (the watchdog's clock; thread 0 of rank 0 only)
 #define TICK(slot) do { if (timer) { unsigned long long t_ = gz2::gtimer(); t_acc[slot] += t_ - t_prev; t_prev = t_; } } while (0)
 #define FOR_TILES for (int tile = g.t0 + cta; tile < g.t1; tile += ncta)
     long long flow = 0, offset = 0, presat = 0, pushes = 0, relabels = 0;
@@ -739,10 +744,10 @@ __device__ __forceinline__ void tilesolve_body(Prob p, Bits2 b, Arr3 a, Geo g, u
         ++sweeps;
         if (p.trace && threadIdx.x == 0 && tm.rank == 0)
             printf("gz_trace sweep %d levels %d pulses %d t %.3f ms bfs %.3f pulses %.3f\n", sweeps, d, pulses,
-                   (gz2::gtimer() - p.t_start_ns) * 1e-6, t_acc[2] * 1e-6, t_acc[3] * 1e-6);
+                   (gz2::gtimer() - t_start) * 1e-6, t_acc[2] * 1e-6, t_acc[3] * 1e-6);
         {
             unsigned stop = 0;
-            if (threadIdx.x == 0 && tm.rank == 0 && gz2_watchdog_expired(p)) stop = 1;
+            if (threadIdx.x == 0 && tm.rank == 0 && p.watchdog_ns && gz2::gtimer() - t_start > p.watchdog_ns) stop = 1;
             if (TEAM_OR(stop)) {
                 if (threadIdx.x == 0 && tm.rank == 0) vctr[CTR_STATUS] = (unsigned long long)(-GZ_ERR_NOCONVERGE);
                 break;
@@ -827,7 +832,12 @@ __device__ __forceinline__ void tilesolve_body(Prob p, Bits2 b, Arr3 a, Geo g, u
 }
 
 template <int LP, int R, bool WIN, int OCC, int RW = 0>
-__global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(Prob p, Bits2 b, Arr3 a, Geo g, unsigned long long *bar) {
+// (__grid_constant__: the body reads the parameters in place, from the constant bank)
+__global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(const __grid_constant__ Prob p,
+                                                                  const __grid_constant__ Bits2 b,
+                                                                  const __grid_constant__ Arr3 a,
+                                                                  const __grid_constant__ Geo g,
+                                                                  unsigned long long *bar) {
     int phase = 0;
     tilesolve_body<LP, R, WIN, OCC, RW>(p, b, a, g, bar, (int)blockIdx.x, (int)gridDim.x, phase);
 }
@@ -859,7 +869,10 @@ template <typename T>
 __device__ __forceinline__ T *shifted(T *q, size_t off) { return q ? (T *)((uint8_t *)q + off) : q; }
 
 template <int LP, int R, int OCC>
-__global__ void __launch_bounds__(BLOCK, OCC) gz_pairs_kernel(Prob p0, Bits2 b0, Arr3 a0, Geo g, PairBatch pb) {
+__global__ void __launch_bounds__(BLOCK, OCC) gz_pairs_kernel(const __grid_constant__ Prob p0,
+                                                              const __grid_constant__ Bits2 b0,
+                                                              const __grid_constant__ Arr3 a0,
+                                                              const __grid_constant__ Geo g, PairBatch pb) {
     const int T = pb.T, team = (int)blockIdx.x / T, cta = (int)blockIdx.x % T;
     const size_t off = (size_t)team * pb.ws_stride;
     Prob p = p0;
@@ -928,8 +941,7 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_pairs_kernel(Prob p0, Bits2 b0,
         unsigned long long t0 = gz2::gtimer();
         Prob q = p;
         q.labels = pb.labels_out + (size_t)pair * P;
-        q.t_start_ns = t0;
-        tilesolve_body<LP, R, false, OCC, 0>(q, b, a, g, bar, cta, T, phase);
+        tilesolve_body<LP, R, false, OCC, 0, Prob, Bits2, Arr3>(q, b, a, g, bar, cta, T, phase);
         __threadfence();
         (void)tm.sync_or(0u, phase, s_t3, s_u3);
         if (cta == 0 && threadIdx.x < CTR_COUNT) {
