@@ -111,16 +111,31 @@ __device__ __forceinline__ BW<NW> andnot(BW<NW> a, const BW<NW> &b) {
 
 // ---------------------------------------------------------------------------
 // extraction on the final masks: reach prefix r (positions lo+1 .. lo+r).
-template <bool WIN, int NW>
+// Arc-mask word (arc q, word w) of site c.  PACK (16-lane chains, NW = 1): the
+// 16-bit masks of arcs 2k and 2k+1 share word k (7 words per site instead of
+// 13: fewer bytes for every mask build, BFS region load and reach pass).
+template <bool PACK, int NW>
+__device__ __forceinline__ uint32_t mask_word(const uint32_t *mask, int P, int q, int w, int c) {
+    if (PACK) return (mask[(size_t)(q >> 1) * P + c] >> ((q & 1) * 16)) & 0xffffu;
+    return mask[((size_t)q * NW + w) * P + c];
+}
+template <bool PACK, int NW>
+__device__ __forceinline__ BW<NW> mask_bw(const uint32_t *mask, int P, int q, int c) {
+    BW<NW> r;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) r.w[w] = mask_word<PACK, NW>(mask, P, q, w, c);
+    return r;
+}
+
+template <bool WIN, int NW, bool PACK = false>
 __device__ int bit_close_up(const Bits2 &b, int P, int c, int lo, int hi, int r) {
     if (r <= 0) return 0;
-    BW<NW> cu;
-    cu.load(b.mask, P, c);
+    const BW<NW> cu = mask_bw<PACK, NW>(b.mask, P, A_UP, c);
     while (lo + r < hi && cu.test(lo + r - 1)) ++r;
     return r;
 }
 
-template <bool WIN, int NW>
+template <bool WIN, int NW, bool PACK = false>
 __device__ bool bit_reach_iter(const Prob &p, const Bits2 &b, int c, const int32_t *Rin, int32_t *Rout) {
     const int P = p.P;
     const int y = c / p.G, g = c - y * p.G;
@@ -141,17 +156,16 @@ __device__ bool bit_reach_iter(const Prob &p, const Bits2 &b, int c, const int32
         const int lon = WIN ? p.lo[nc[i]] : 0;
         BW<NW> Rn = BW<NW>::range(lon, lon + rn);
         const int j = i ^ 1;   // direction from the neighbour back to c
-        BW<NW> s, dd, uu;
-        s.load(b.mask + (size_t)(A_SR + j) * NW * P, P, nc[i]);
-        dd.load(b.mask + (size_t)(A_DR + j) * NW * P, P, nc[i]);
-        uu.load(b.mask + (size_t)(A_UR + j) * NW * P, P, nc[i]);
+        const BW<NW> s = mask_bw<PACK, NW>(b.mask, P, A_SR + j, nc[i]);
+        const BW<NW> dd = mask_bw<PACK, NW>(b.mask, P, A_DR + j, nc[i]);
+        const BW<NW> uu = mask_bw<PACK, NW>(b.mask, P, A_UR + j, nc[i]);
         T = T | (Rn & s) | (Rn & dd).shr1() | (Rn & uu).shl1();
         anyn = true;
     }
     if (anyn) {
         T = T & BW<NW>::range(lo, hi);
         const int top = T.top();
-        if (top >= 0 && top + 1 - lo > r) r = bit_close_up<WIN, NW>(b, P, c, lo, hi, top + 1 - lo);
+        if (top >= 0 && top + 1 - lo > r) r = bit_close_up<WIN, NW, PACK>(b, P, c, lo, hi, top + 1 - lo);
     }
     Rout[c] = r;
     return r != r0;

@@ -489,7 +489,13 @@ __device__ void w_build(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
         }
     } else if (!RW && L.valid && L.j == 0) {
 #pragma unroll
-        for (int q = 0; q < 13; ++q) b.mask[((size_t)q * R + L.s) * P + L.c] = m[q];
+        if (LP == 16 && R == 1) {   // packed 16-bit masks (gz_bits.cuh mask_word)
+#pragma unroll
+            for (int q = 0; q < 13; q += 2) b.mask[(size_t)(q >> 1) * P + L.c] = m[q] | (q + 1 < 13 ? m[q + 1] << 16 : 0u);
+        } else {
+#pragma unroll
+            for (int q = 0; q < 13; ++q) b.mask[((size_t)q * R + L.s) * P + L.c] = m[q];
+        }
         b.EX[L.wi] = ex;
         b.V[L.wi] = 0u;
         b.A[L.wi] = 0u;
@@ -777,7 +783,7 @@ __device__ void w_commit(const Prob &p, const Arr3 &a, const Bits2 &b, int c_bas
 }
 
 // extraction seeds: highest position holding excess (last mask build's words)
-template <int R, bool WIN>
+template <int R, bool WIN, bool PACK = false>
 __device__ void w_reach_init(const Prob &p, const Bits2 &b, int c) {
     int lo = 0, hi = p.L;
     if (WIN) { lo = p.lo[c]; hi = p.hi[c]; }
@@ -785,7 +791,7 @@ __device__ void w_reach_init(const Prob &p, const Bits2 &b, int c) {
     ex.load(b.EX, p.P, c);
     const int top = ex.top();
     const int r = top >= 0 ? top + 1 - lo : 0;
-    b.R0[c] = gz2::bit_close_up<WIN, R>(b, p.P, c, lo, hi, r);
+    b.R0[c] = gz2::bit_close_up<WIN, R, PACK>(b, p.P, c, lo, hi, r);
 }
 
 template <int LPT>

@@ -171,6 +171,7 @@ __device__ unsigned bfs_round(const Prob &p, const Arr3 &a, const Bits2 &b, cons
                               const uint32_t *Fin, uint32_t *Fout, const uint32_t *Vin, uint32_t *Vout, int d,
                               uint32_t *sF0, uint32_t *sF1, uint32_t *sM, bool load_masks, bool &front) {
     constexpr int RS = region_sites(NW, OCC), SPT = RS / BLOCK;
+    constexpr bool PACK = LPT == 16;   // 16-lane chains: packed arc masks (gz_bits.cuh mask_word)
     const int P = p.P, H = g.H;
     const int ry0 = max(tb.y0 - H, 0), ry1 = min(tb.y1 + H, p.Y);
     const int rx0 = max(tb.x0 - H, 0), rx1 = min(tb.x1 + H, p.G);
@@ -191,7 +192,7 @@ __device__ unsigned bfs_round(const Prob &p, const Arr3 &a, const Bits2 &b, cons
         NB[k] = (rj + 1 < RW ? 1u : 0u) | (rj > 0 ? 2u : 0u) | (i + RW < nreg ? 4u : 0u) | (ri > 0 ? 8u : 0u);
         if (smem_masks(NW) && load_masks && ok) {
 #pragma unroll
-            for (int q = 0; q < 13 * NW; ++q) sM[q * RS + i] = b.mask[(size_t)q * P + c];
+            for (int q = 0; q < (PACK ? 7 : 13 * NW); ++q) sM[q * RS + i] = b.mask[(size_t)q * P + c];
         }
         V[k].zero(); EX[k].zero(); RNG[k].zero();
         if (ok) {
@@ -230,7 +231,8 @@ __device__ unsigned bfs_round(const Prob &p, const Arr3 &a, const Bits2 &b, cons
                 continue;
             }
             // mask word (arc q, word w) of this site: shared memory, or global memory (NW = 8)
-#define GZ_MASK(q, w) (smem_masks(NW) ? sM[((q) * NW + (w)) * RS + i] : __ldg(b.mask + ((size_t)(q) * NW + (w)) * P + C[k]))
+#define GZ_MASK(q, w) (PACK ? ((sM[((q) >> 1) * RS + i] >> (((q) & 1) * 16)) & 0xffffu) \
+                     : smem_masks(NW) ? sM[((q) * NW + (w)) * RS + i] : __ldg(b.mask + ((size_t)(q) * NW + (w)) * P + C[k]))
             BW<NW> M0;
 #pragma unroll
             for (int w = 0; w < NW; ++w) M0.w[w] = GZ_MASK(A_UP, w);
@@ -768,13 +770,13 @@ __device__ __forceinline__ void tilesolve_body(PP p, BB b, AA a, const Geo &g, u
     // preflow converges).  Reaching the sink is closed upward along a chain
     // (uncuttable chain arcs down), so the source side is a prefix.
     const bool capped_stop = v_last != nullptr;
-    if (!capped_stop) FOR_TILE_SITES gz3::w_reach_init<NW, WIN>(p, b, r * p.G + x);
+    if (!capped_stop) FOR_TILE_SITES gz3::w_reach_init<NW, WIN, LPT == 16>(p, b, r * p.G + x);
     TEAM_SYNC();
     int reach_passes = 0;
     int32_t *Rin = b.R0, *Rout = b.R1;
     for (; !capped_stop;) {
         unsigned ch = 0;
-        FOR_TILE_SITES ch |= gz2::bit_reach_iter<WIN, NW>(p, b, r * p.G + x, Rin, Rout) ? 1u : 0u;
+        FOR_TILE_SITES ch |= gz2::bit_reach_iter<WIN, NW, LPT == 16>(p, b, r * p.G + x, Rin, Rout) ? 1u : 0u;
         const bool any = TEAM_OR(ch) != 0;
         int32_t *t = Rin; Rin = Rout; Rout = t;
         ++reach_passes;
