@@ -136,14 +136,14 @@ __device__ int bit_close_up(const Bits2 &b, int P, int c, int lo, int hi, int r)
 }
 
 template <bool WIN, int NW, bool PACK = false>
-__device__ bool bit_reach_iter(const Prob &p, const Bits2 &b, int c, const int32_t *Rin, int32_t *Rout) {
+__device__ bool bit_reach_iter(const Prob &p, const Bits2 &b, int c, int32_t *R) {
     const int P = p.P;
     const int y = c / p.G, g = c - y * p.G;
     const bool has[4] = {g + 1 < p.G, g > 0, y + 1 < p.Y, y > 0};
     const int nc[4] = {c + 1, c - 1, c + p.G, c - p.G};
     int lo = 0, hi = p.L;
     if (WIN) { lo = p.lo[c]; hi = p.hi[c]; }
-    const int r0 = Rin[c];
+    const int r0 = R[c];
     int r = r0;
     BW<NW> T;
     T.zero();
@@ -151,7 +151,7 @@ __device__ bool bit_reach_iter(const Prob &p, const Bits2 &b, int c, const int32
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         if (!has[i]) continue;
-        const int rn = Rin[nc[i]];
+        const int rn = R[nc[i]];
         if (rn <= 0) continue;
         const int lon = WIN ? p.lo[nc[i]] : 0;
         BW<NW> Rn = BW<NW>::range(lon, lon + rn);
@@ -167,8 +167,9 @@ __device__ bool bit_reach_iter(const Prob &p, const Bits2 &b, int c, const int32
         const int top = T.top();
         if (top >= 0 && top + 1 - lo > r) r = bit_close_up<WIN, NW, PACK>(b, P, c, lo, hi, top + 1 - lo);
     }
-    Rout[c] = r;
-    return r != r0;
+    if (r == r0) return false;
+    R[c] = r;   // in place: see the reach loop in gz_tilesolve.cuh
+    return true;
 }
 
 // ---------------------------------------------------------------------------

@@ -773,12 +773,15 @@ __device__ __forceinline__ void tilesolve_body(PP p, BB b, AA a, const Geo &g, u
     if (!capped_stop) FOR_TILE_SITES gz3::w_reach_init<NW, WIN, LPT == 16>(p, b, r * p.G + x);
     TEAM_SYNC();
     int reach_passes = 0;
-    int32_t *Rin = b.R0, *Rout = b.R1;
+    // In place (Gauss-Seidel): R only grows and every value a pass reads is a
+    // lower bound of the fixpoint, so a read of a neighbour already updated in
+    // this pass is as valid as the old one and converges in fewer passes; a
+    // pass that changes nothing read only settled values, i.e. the fixpoint.
+    int32_t *const Rin = b.R0;
     for (; !capped_stop;) {
         unsigned ch = 0;
-        FOR_TILE_SITES ch |= gz2::bit_reach_iter<WIN, NW, LPT == 16>(p, b, r * p.G + x, Rin, Rout) ? 1u : 0u;
+        FOR_TILE_SITES ch |= gz2::bit_reach_iter<WIN, NW, LPT == 16>(p, b, r * p.G + x, Rin) ? 1u : 0u;
         const bool any = TEAM_OR(ch) != 0;
-        int32_t *t = Rin; Rin = Rout; Rout = t;
         ++reach_passes;
         if (!any) break;
         if (reach_passes > 4 * (p.P + p.M)) { if (threadIdx.x == 0 && tm.rank == 0) vctr[CTR_STATUS] = (unsigned long long)(-GZ_ERR_NOCONVERGE); break; }
