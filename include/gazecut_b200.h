@@ -120,7 +120,10 @@ int gz_solve_volume(const int32_t *vol, int32_t rows, int32_t cols, int32_t m, c
  * runs up to k pair solves at once.  m <= 16 (BASELINE config 4): ONE launch
  * of teams of GZ_PAIR_TEAM (2) CTAs, team k on workspace slice k, pairs handed
  * out by a device queue (gz4::gz_pairs_kernel; size the workspace with
- * gz_pairs_workspace_bytes).  Otherwise up to GZ_PAIR_CONC (8) cooperative
+ * gz_pairs_workspace_bytes); for batches of at least four pairs per team the
+ * last twelfth of the pairs go to a second launch of 8-CTA teams on another
+ * stream, issued when the first launch's queue runs dry (GZ_PAIR_TAIL /
+ * GZ_PAIR_TEAM2 override; gz_pairs_launches).  Otherwise up to GZ_PAIR_CONC (8) cooperative
  * launches over 1/k of the SMs each, one stream per slice.  At least one
  * slice is required.  Calls on one device are serialised (a per-device lock
  * guards the stream pool and the pinned counter buffer). */
@@ -134,6 +137,12 @@ int gz_solve_pairs(const uint8_t *left, const uint8_t *right, int32_t batch, int
  * batched launch, GZ_PAIR_TEAM CTAs per team; otherwise GZ_PAIR_CONC slices).
  * Queries the current device; 0 on error. */
 size_t gz_pairs_workspace_bytes(int32_t rows, int32_t cols, int32_t m, int32_t batch);
+
+/* Kernel launches gz_solve_pairs makes for `batch` pairs of this shape with a
+ * workspace of workspace_bytes on the current device: 1 or 2 (the batched
+ * launch, plus its tail launch), or -1 when the batch takes the per-pair
+ * launch path (m > 16).  Negative gz_status on error. */
+int gz_pairs_launches(int32_t rows, int32_t cols, int32_t m, int32_t batch, size_t workspace_bytes);
 
 /* Same as gz_solve_pairs with HOST buffers (pinned or pageable): copies in,
  * solves, copies labels out.  The reference-facing end-to-end call. */

@@ -8,10 +8,11 @@ library or an sm_100 GPU is missing, every solver entry point raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 PKG_DIR = Path(__file__).resolve().parent
-LIB_PATH = PKG_DIR / "libgazecut_b200.so"
+LIB_PATH = Path(os.environ["GZ_LIB_PATH"]) if os.environ.get("GZ_LIB_PATH") else PKG_DIR / "libgazecut_b200.so"   # (A/B runs)
 
 GZ_OK = 0
 GZ_ERR_ARG = -1
@@ -103,6 +104,8 @@ def lib():
                                      _vp, C.c_size_t, _vp]
         L.gz_pairs_workspace_bytes.restype = C.c_size_t
         L.gz_pairs_workspace_bytes.argtypes = [_i32, _i32, _i32, _i32]
+        L.gz_pairs_launches.restype = C.c_int
+        L.gz_pairs_launches.argtypes = [_i32, _i32, _i32, _i32, C.c_size_t]
         L.gz_solve_pairs_host.restype = C.c_int
         L.gz_solve_pairs_host.argtypes = L.gz_solve_pairs.argtypes
         L.gz_solve_volume_banded.restype = C.c_int
@@ -161,7 +164,7 @@ def check(status: int, where: str) -> None:
 
 # Every symbol include/gazecut_b200.h declares (checked by tests/test_abi.py).
 EXPORTED = (
-    "gz_workspace_bytes", "gz_sad_volume", "gz_solve_volume", "gz_solve_pairs", "gz_pairs_workspace_bytes",
+    "gz_workspace_bytes", "gz_sad_volume", "gz_solve_volume", "gz_solve_pairs", "gz_pairs_workspace_bytes", "gz_pairs_launches",
     "gz_solve_pairs_host", "gz_solve_volume_banded", "gz_ground_truth_to_depth",
     "gz_error_count", "gz_render_disparity", "gz_solve_volume_batch", "gz_total_energy", "gz_coarsen", "gz_thin_skin",
     "gz_status_string", "gz_build_info", "gz_export_arcs", "gz_export_state", "gz_csr_workspace_bytes",

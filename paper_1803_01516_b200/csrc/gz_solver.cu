@@ -22,7 +22,9 @@
 #include <ctime>
 #include <unistd.h>
 
+#include <chrono>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "gz_common.cuh"
@@ -802,6 +804,13 @@ struct DevicePool {
         have_streams = true;
         return GZ_OK;
     }
+    unsigned *flag_host = nullptr, *flag_dev = nullptr;   // host-mapped word (batched tail launch)
+    int flag_ready() {
+        if (flag_host) return GZ_OK;
+        CK(cudaHostAlloc((void **)&flag_host, 256, cudaHostAllocMapped));
+        CK(cudaHostGetDevicePointer((void **)&flag_dev, flag_host, 0));
+        return GZ_OK;
+    }
     int pinned_ready(size_t n) {
         if (pinned_n >= n) return GZ_OK;
         if (pinned) cudaFreeHost(pinned);
@@ -1254,23 +1263,59 @@ int pair_teams(int m) {
 // nteams x T CTAs, team k on workspace slice k, pairs handed out by a device
 // queue.  One-CTA teams (T = 1, the default) synchronise with CTA barriers
 // only and keep up to 2 x 148 pairs in flight.
+// The launch plan of a batched solve: teams of T CTAs in one cooperative launch
+// (as many as fit the SMs and the workspace), then -- for batches of at least
+// four pairs per team -- a tail launch of T2-CTA teams for the last `tail`
+// pairs (gz_tilesolve.cuh PairBatch; 1184 C1 pairs: ~1575 -> ~1500 ms per
+// batch, profiles/r2_runs/tail_launch.txt).
+struct PairsPlan {
+    int occ, T, nteams, T2, nt2, tail;
+    const void *kern;
+    size_t dyn;
+};
+
+int plan_pairs(int rows, int cols, int m, int batch, size_t workspace_bytes, int T, PairsPlan &pl) {
+    const size_t one = ws_bytes(rows, cols, m);
+    pl.T = T;
+    pl.occ = 2;
+    if (const char *oc = getenv("GZ_OCC")) pl.occ = atoi(oc) == 1 ? 1 : 2;
+    pl.kern = gz4::pairs_kernel_lp16(pl.occ);
+    pl.dyn = gz4::smem_bytes(pl.occ);
+    CK(cudaFuncSetAttribute(pl.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.dyn));
+    int grid = 0;
+    int rc = coop_grid(pl.kern, gz4::BLOCK, &grid, pl.dyn);
+    if (rc) return rc;
+    int nteams = grid / T;
+    if ((size_t)nteams * one > workspace_bytes) nteams = (int)(workspace_bytes / one);
+    if (nteams > batch) nteams = batch;
+    if (const char *e = getenv("GZ_PAIR_TEAMS"))   // (tests: fewer teams than pairs on small batches)
+        if (atoi(e) > 0 && atoi(e) < nteams) nteams = atoi(e);
+    if (nteams < 1) return GZ_ERR_WORKSPACE;
+    pl.nteams = nteams;
+    int T2 = 8, tail = batch >= 4 * nteams ? batch / 12 : 0;
+    if (const char *e = getenv("GZ_PAIR_TEAM2")) T2 = atoi(e);
+    if (const char *e = getenv("GZ_PAIR_TAIL")) tail = atoi(e);
+    const int nt2 = T2 > T ? nteams * T / T2 : 0;   // T2 > T: never more tail teams than slices
+    if (nt2 < 1 || tail < 0) tail = 0;
+    if (tail > batch - nteams) tail = batch - nteams > 0 ? batch - nteams : 0;
+    pl.T2 = T2;
+    pl.nt2 = nt2;
+    pl.tail = tail;
+    return GZ_OK;
+}
+
 int solve_pairs_batched(const uint8_t *left, const uint8_t *right, int batch, int img_h, int img_w, int channels,
                         const gz_cuboid *cb, const gz_energy *energy, const gz_sched *sched, int32_t *labels_out,
                         gz_stats *stats_out, void *workspace, size_t workspace_bytes, cudaStream_t s, int T) {
     const int rows = cb->y_extent, cols = cb->g_extent, m = cb->m, P = rows * cols;
     const size_t one = ws_bytes(rows, cols, m);
-    int occ = 2;
-    if (const char *oc = getenv("GZ_OCC")) occ = atoi(oc) == 1 ? 1 : 2;
-    const void *kern = gz4::pairs_kernel_lp16(occ);
-    const size_t dyn = gz4::smem_bytes(occ);
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-    int grid = 0;
-    int rc = coop_grid(kern, gz4::BLOCK, &grid, dyn);
+    PairsPlan pl;
+    int rc = plan_pairs(rows, cols, m, batch, workspace_bytes, T, pl);
     if (rc) return rc;
-    int nteams = grid / T;
-    if ((size_t)nteams * one > workspace_bytes) nteams = (int)(workspace_bytes / one);
-    if (nteams > batch) nteams = batch;
-    if (nteams < 1) return GZ_ERR_WORKSPACE;
+    const int occ = pl.occ, nteams = pl.nteams, T2 = pl.T2, nt2 = pl.nt2, tail = pl.tail;
+    const void *kern = pl.kern;
+    const size_t dyn = pl.dyn;
+    int grid = 0;
     Workspace w = carve(workspace, rows, cols, m);
     Prob p;
     gz_sched sc = sched ? *sched : gz_sched{12, 0, 0, 0};
@@ -1296,28 +1341,79 @@ int solve_pairs_batched(const uint8_t *left, const uint8_t *right, int batch, in
     pb.labels_out = labels_out;
     unsigned long long *dbuf = nullptr;
     const size_t sbytes = (size_t)batch * gz::CTR_COUNT * 8;
-    CK(cudaMallocAsync((void **)&dbuf, sbytes + 256, s));
+    // tail launch (gz_tilesolve.cuh PairBatch): the last `tail` pairs go to a
+    // second launch of T2-CTA teams, issued once the first launch's queue is dry
+    const int grid1 = nteams * T, batch1 = batch - tail;
+    const size_t tbytes = align_up((size_t)nteams * 4) * 2 + align_up((size_t)(nt2 > 0 ? nt2 : 1) * 4) + 256;
+    CK(cudaMallocAsync((void **)&dbuf, sbytes + 256 + tbytes, s));
     pb.stats = dbuf;
     pb.queue = (unsigned *)((uint8_t *)dbuf + sbytes);
-    CK(cudaMemsetAsync(pb.queue, 0, 16, s));
+    uint8_t *tb = (uint8_t *)dbuf + sbytes + 256;
+    pb.done = (unsigned *)tb;
+    pb.free_slices = tail ? (int *)(tb + align_up((size_t)nteams * 4)) : nullptr;
+    pb.pub = (int *)(tb + 2 * align_up((size_t)nteams * 4));
+    pb.free_n = (unsigned *)(tb + 2 * align_up((size_t)nteams * 4) + align_up((size_t)(nt2 > 0 ? nt2 : 1) * 4));
+    CK(cudaMemsetAsync(pb.queue, 0, 256 + tbytes, s));
+    if (tail) CK(cudaMemsetAsync(pb.free_slices, 0xff, (size_t)nteams * 4, s));
+    pb.lo = 0;
+    pb.batch = batch1;
+    pb.tail = 0;
+    pb.drained = nullptr;
     // team barrier words and counters of every slice start clear
     for (int k = 0; k < nteams; ++k) {
         Workspace wk = carve((uint8_t *)workspace + (size_t)k * one, rows, cols, m);
         CK(cudaMemsetAsync(wk.ctr, 0, gz::CTR_COUNT * 8, s));
     }
-    void *args[] = {&p, &bb, &a3, &geo, &pb};
-    grid = nteams * T;
-    CK(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(gz4::BLOCK), args, dyn, s));
     DevicePool *pool = device_pool();
     if (!pool) return GZ_ERR_CUDA;
     std::lock_guard<std::mutex> lock(pool->mu);
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    if (tail) {
+        if ((rc = pool->flag_ready()) || (rc = pool->streams_ready())) return rc;
+        *(volatile unsigned *)pool->flag_host = 0u;
+        pb.drained = pool->flag_dev;
+        s2 = pool->streams[0] == s ? pool->streams[1] : pool->streams[0];
+        CK(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ev1, cudaEventDisableTiming));
+        CK(cudaEventRecord(ev0, s));   // the tail launch follows this call's memsets
+        CK(cudaStreamWaitEvent(s2, ev0, 0));
+    }
+    void *args[] = {&p, &bb, &a3, &geo, &pb};
+    grid = grid1;
+    CK(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(gz4::BLOCK), args, dyn, s));
+    gz4::Geo geo2 = geo;
+    if (tail) {
+        gz4::PairBatch pb2 = pb;
+        pb2.T = T2;
+        pb2.lo = batch1;
+        pb2.batch = batch;
+        pb2.queue = pb.queue + 1;
+        pb2.tail = 1;
+        pb2.drained = nullptr;
+        geo2 = tile_geo(rows, cols, T2, words_for(m), occ);
+        // wait until the first launch's queue is dry (or the launch is over),
+        // then launch the tail teams behind it on a second stream
+        while (!*(volatile unsigned *)pool->flag_host) {
+            const cudaError_t q = cudaStreamQuery(s);
+            if (q == cudaSuccess) break;
+            if (q != cudaErrorNotReady) return GZ_ERR_CUDA;
+            std::this_thread::sleep_for(std::chrono::microseconds(50));
+        }
+        void *args2[] = {&p, &bb, &a3, &geo2, &pb2};
+        CK(cudaLaunchKernel(kern, dim3(nt2 * T2), dim3(gz4::BLOCK), args2, dyn, s2));
+        CK(cudaEventRecord(ev1, s2));
+        CK(cudaStreamWaitEvent(s, ev1, 0));
+        cudaEventDestroy(ev0);
+        cudaEventDestroy(ev1);
+    }
     if ((rc = pool->pinned_ready((size_t)batch * gz::CTR_COUNT))) return rc;
     CK(cudaMemcpyAsync(pool->pinned, dbuf, sbytes, cudaMemcpyDeviceToHost, s));
     cudaFreeAsync(dbuf, s);
     CK(cudaStreamSynchronize(s));
     for (int b = 0; b < batch && rc == GZ_OK; ++b) {
         const unsigned long long *h = pool->pinned + (size_t)b * gz::CTR_COUNT;
-        rc = stats_from_ctr(h, energy->hard_inhibit ? 1 : 0, 1 << 30, (float)(h[CTR_NS] * 1e-6), geo.H,
+        rc = stats_from_ctr(h, energy->hard_inhibit ? 1 : 0, 1 << 30, (float)(h[CTR_NS] * 1e-6), b < batch1 ? geo.H : geo2.H,
                             stats_out ? stats_out + b : nullptr);
     }
     if (rc) return rc;
@@ -1616,6 +1712,17 @@ int gz_thin_skin(const int32_t *coarse_labels, int32_t crows, int32_t ccols, int
                                                                   radius, lo_out, hi_out);
     CK(cudaGetLastError());
     return GZ_OK;
+}
+
+int gz_pairs_launches(int32_t rows, int32_t cols, int32_t m, int32_t batch, size_t workspace_bytes) {
+    if (rows < 1 || cols < 1 || m < 2 || batch < 1 || !index_fits(rows, cols, m)) return GZ_ERR_ARG;
+    int rc = check_sm100();
+    if (rc) return rc;
+    const int T = pair_team();
+    if (choose_solver(m, nullptr) != 4 || lanes_for(m) != 16 || T < 1) return -1;
+    PairsPlan pl;
+    if ((rc = plan_pairs(rows, cols, m, batch, workspace_bytes, T, pl))) return rc;
+    return pl.tail ? 2 : 1;
 }
 
 size_t gz_pairs_workspace_bytes(int32_t rows, int32_t cols, int32_t m, int32_t batch) {

@@ -857,17 +857,34 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_tilesolve_kernel(const __grid_c
 // cross-SM barriers (T = 1: the CTA barrier is the team barrier) and keep many
 // pairs in flight; one launch avoids the per-stream concurrency limit of
 // separate cooperative launches (CUDA_DEVICE_MAX_CONNECTIONS).
+//
+// Tail launch: small teams are the most efficient per CTA, but once the queue
+// runs dry a team that finishes early idles until the slowest pair in flight
+// is done.  The last pairs therefore go to a SECOND launch of bigger teams
+// (T2 CTAs), issued on another stream as soon as the first launch's queue is
+// empty (the first launch raises a host-visible flag; the host then launches):
+// its CTAs take the SM slots the first launch's CTAs free as they exit.  It
+// cannot deadlock -- the first launch is fully resident by then and never
+// waits on the second -- and a tail team works in the workspace slice of a
+// finished small team (released once all its CTAs are done, `free`).
 struct PairBatch {
     const uint8_t *left, *right;   // batch x (img_h, img_w, ch) uint8
     int img_w, ch;
     size_t img_bytes;
     gz_cuboid cb;
-    int batch, T;
+    int batch, T;                   // this launch hands out pairs [lo, batch)
     size_t ws_stride;               // bytes between two teams' workspace slices
     size_t bits_bytes;              // bytes of the bit planes to clear per pair
     int32_t *labels_out;            // batch x P
     unsigned long long *stats;      // batch x CTR_COUNT counters
-    unsigned *queue;                // next pair to hand out
+    unsigned *queue;                // next pair to hand out (relative to lo)
+    int lo;
+    int tail;                       // 0: first launch (slice = team); 1: tail launch (slices from `free`)
+    unsigned *drained;              // host-mapped: set when the first launch's queue runs dry (or nullptr)
+    unsigned *done;                 // first launch: per team, CTAs done
+    int *free_slices;               // released slices, in release order (-1: not yet)
+    unsigned *free_n;               // [0] released, [1] taken
+    int *pub;                       // tail launch: per team, 1 + its slice
 };
 
 template <typename T>
@@ -879,7 +896,31 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_pairs_kernel(const __grid_const
                                                               const __grid_constant__ Arr3 a0,
                                                               const __grid_constant__ Geo g, PairBatch pb) {
     const int T = pb.T, team = (int)blockIdx.x / T, cta = (int)blockIdx.x % T;
-    const size_t off = (size_t)team * pb.ws_stride;
+    size_t off = (size_t)team * pb.ws_stride;
+    if (pb.tail) {
+        // a tail team takes the next released slice (CTA 0) and clears its
+        // barrier words and pair slot before the team's first barrier
+        __shared__ int s_slice;
+        if (threadIdx.x == 0) {
+            int sl;
+            if (cta == 0) {
+                const unsigned k = atomicAdd(pb.free_n + 1, 1u);
+                while ((sl = *(volatile int *)&pb.free_slices[k]) < 0) __nanosleep(1000);
+                __threadfence();
+                unsigned long long *c = (unsigned long long *)((uint8_t *)p0.ctr + (size_t)sl * pb.ws_stride);
+                for (int i = 0; i < CTR_COUNT; ++i) ((volatile unsigned long long *)c)[i] = 0ull;
+                __threadfence();
+                *(volatile int *)&pb.pub[team] = sl + 1;
+            } else {
+                while ((sl = *(volatile int *)&pb.pub[team]) == 0) __nanosleep(1000);
+                sl -= 1;
+                __threadfence();
+            }
+            s_slice = sl;
+        }
+        __syncthreads();
+        off = (size_t)s_slice * pb.ws_stride;
+    }
     Prob p = p0;
     p.vol = shifted(p.vol, off); p.cu = shifted(p.cu, off); p.ph = shifted(p.ph, off); p.pv = shifted(p.pv, off);
     p.dar = shifted(p.dar, off); p.dbr = shifted(p.dbr, off); p.dad = shifted(p.dad, off); p.dbd = shifted(p.dbd, off);
@@ -906,9 +947,13 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_pairs_kernel(const __grid_const
     for (;;) {
         // ---- next pair: CTA 0 of the team draws it, the team barrier publishes it ----
         if (cta == 0 && threadIdx.x == 0) {
-            const int k = (int)atomicAdd(pb.queue, 1u);
+            const int k = pb.lo + (int)atomicAdd(pb.queue, 1u);
             if (T == 1) s_pair = k;
             else *(volatile int *)&p.ctr[CTR_PAIR] = k;
+            if (k >= pb.batch && pb.drained && !*(volatile unsigned *)pb.drained) {
+                *(volatile unsigned *)pb.drained = 1u;   // the host may launch the tail now
+                __threadfence_system();
+            }
         }
         (void)tm.sync_or(0u, phase, s_t3, s_u3);
         const int pair = T == 1 ? s_pair : *(volatile int *)&p.ctr[CTR_PAIR];
@@ -953,6 +998,15 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_pairs_kernel(const __grid_const
             unsigned long long v = ((volatile unsigned long long *)p.ctr)[threadIdx.x];
             if (threadIdx.x == CTR_NS) v = gz2::gtimer() - t0;
             pb.stats[(size_t)pair * CTR_COUNT + threadIdx.x] = v;
+        }
+    }
+    // first launch with a tail launch behind it: the last of the team's CTAs to
+    // finish releases the slice (no CTA of the team touches it afterwards)
+    if (!pb.tail && pb.free_slices && threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&pb.done[team], 1u) == (unsigned)(T - 1)) {
+            const unsigned k = atomicAdd(pb.free_n, 1u);
+            *(volatile int *)&pb.free_slices[k] = team;
         }
     }
 }

@@ -62,6 +62,15 @@ class PairSolver:
             self._ws = torch.empty(need, dtype=torch.uint8, device=self.dev)
         return self._ws
 
+    def launches(self, batch: int) -> int:
+        """Kernel launches one ``solve`` of ``batch`` pairs makes (1, or 2 with the
+        batched tail launch; -1: the per-pair launch path)."""
+        y, g, m = self.cuboid.y_extent, self.cuboid.g_extent, self.cuboid.num_labels
+        n = _lib.lib().gz_pairs_launches(y, g, m, int(batch), self._workspace(0, batch).numel())
+        if n < -1:
+            _lib.check(n, "gz_pairs_launches")
+        return n
+
     def solve(self, left: torch.Tensor, right: torch.Tensor, labels: Optional[torch.Tensor] = None):
         """Device batch (B, h, w, ch) uint8 -> labels (B, y_extent, g_extent) int32 + per-pair stats."""
         if left.dim() == 3:

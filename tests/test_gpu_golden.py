@@ -122,6 +122,48 @@ def test_pair_batches_every_team_size(gz, monkeypatch, team):
         assert sha(labels[seed].cpu().numpy()) == want["labeling"], (team, seed)
 
 
+@pytest.mark.parametrize("team,teams,tail,team2", [("2", "3", "4", "3"), ("1", "4", "5", "2"), ("2", "2", "6", "4")])
+def test_pair_batches_tail_teams(gz, monkeypatch, team, teams, tail, team2):
+    """The batched launch's tail phase: the last pairs go to bigger teams formed
+    on the fly by the CTAs that found the first queue empty (gz_pairs_kernel).
+    Few teams (GZ_PAIR_TEAMS) so that both phases run on 8 C1 pairs: the
+    reference's fixtures bit for bit, whichever phase solved a pair."""
+    monkeypatch.setenv("GZ_PAIR_TEAM", team)
+    monkeypatch.setenv("GZ_PAIR_TEAMS", teams)
+    monkeypatch.setenv("GZ_PAIR_TAIL", tail)
+    monkeypatch.setenv("GZ_PAIR_TEAM2", team2)
+    cub = gz.cuboid_from_disparity_range(384, 288, 10, 28, num_labels=16)
+    scenes = [gz.make_scene(s) for s in range(8)]
+    left = torch.from_numpy(np.stack([s.left for s in scenes]))
+    right = torch.from_numpy(np.stack([s.right for s in scenes]))
+    solver = gz.PairSolver(cub, gz.EnergyParams(14, 1023), 288, 384, 3)
+    labels, stats = solver.solve(left, right)
+    for seed, want in enumerate(G["c1_exact"]):
+        assert stats[seed]["flow"] == want["flow"], (team, tail, seed)
+        assert sha(labels[seed].cpu().numpy()) == want["labeling"], (team, tail, seed)
+        assert stats[seed]["energy"] == stats[seed]["labeling_energy"]
+
+
+@pytest.mark.parametrize("hard", [False, True])
+def test_pair_batches_tail_small_scenes_match_oracle(gz, oracle, monkeypatch, hard):
+    """Tail teams on small scenes (m = 6) and hard inhibit, against the oracle."""
+    monkeypatch.setenv("GZ_PAIR_TEAM", "1")
+    monkeypatch.setenv("GZ_PAIR_TEAMS", "4")
+    monkeypatch.setenv("GZ_PAIR_TAIL", "6")
+    monkeypatch.setenv("GZ_PAIR_TEAM2", "2")
+    cub = gz.cuboid_from_disparity_range(64, 32, 2, 9, num_labels=6)
+    p = gz.EnergyParams(5, 40, hard)
+    scenes = [gz.make_scene(s, 64, 32, 2, 9) for s in range(12)]
+    left = torch.from_numpy(np.stack([s.left for s in scenes]))
+    right = torch.from_numpy(np.stack([s.right for s in scenes]))
+    labels, stats = gz.PairSolver(cub, p, 32, 64, 3).solve(left, right)
+    for i, s in enumerate(scenes):
+        vol = oracle.sad_volume(s.left, s.right, cub.g_min, cub.g_extent, cub.y_min, cub.y_extent, cub.d_min, 6)
+        want = oracle.solve_exact(vol, 5, 40, hard)
+        assert stats[i]["flow"] == want["flow"] and stats[i]["energy"] == want["energy"], (i, hard)
+        assert np.array_equal(labels[i].cpu().numpy(), want["labeling"]), (i, hard)
+
+
 @pytest.mark.parametrize("hard", [False, True])
 def test_pair_batches_small_scenes_match_oracle(gz, oracle, hard):
     """Batched pairs on small scenes (m = 6, grey and colour) and hard inhibit,
