@@ -144,6 +144,27 @@ def test_pair_batches_tail_teams(gz, monkeypatch, team, teams, tail, team2):
         assert stats[seed]["energy"] == stats[seed]["labeling_energy"]
 
 
+def test_pair_batches_default_tail_rule(gz, monkeypatch):
+    """The default tail rule (a twelfth of a batch of >= 4 pairs per team, teams
+    of 8): 24 C1 pairs on 4 two-CTA teams take two launches, and every pair's
+    flow and labeling equal the single-launch solve's (and the fixtures)."""
+    monkeypatch.setenv("GZ_PAIR_TEAM", "2")
+    monkeypatch.setenv("GZ_PAIR_TEAMS", "4")
+    cub = gz.cuboid_from_disparity_range(384, 288, 10, 28, num_labels=16)
+    scenes = [gz.make_scene(s) for s in range(24)]
+    left = torch.from_numpy(np.stack([s.left for s in scenes]))
+    right = torch.from_numpy(np.stack([s.right for s in scenes]))
+    solver = gz.PairSolver(cub, gz.EnergyParams(14, 1023), 288, 384, 3)
+    assert solver.launches(24) == 2 and solver.launches(8) == 1
+    lab_t, st_t = solver.solve(left, right)
+    monkeypatch.setenv("GZ_PAIR_TAIL", "0")
+    lab_1, st_1 = solver.solve(left, right)
+    assert torch.equal(lab_t, lab_1)
+    assert [s["flow"] for s in st_t] == [s["flow"] for s in st_1]
+    for seed, want in enumerate(G["c1_exact"]):
+        assert st_t[seed]["flow"] == want["flow"] and sha(lab_t[seed].cpu().numpy()) == want["labeling"]
+
+
 @pytest.mark.parametrize("hard", [False, True])
 def test_pair_batches_tail_small_scenes_match_oracle(gz, oracle, monkeypatch, hard):
     """Tail teams on small scenes (m = 6) and hard inhibit, against the oracle."""
