@@ -189,7 +189,11 @@ __device__ unsigned bfs_round(const Prob &p, const Arr3 &a, const Bits2 &b, cons
         const int c = y * p.G + x;
         C[k] = ok ? c : -1;
         IN_[k] = ok && y >= tb.y0 && y < tb.y1 && x >= tb.x0 && x < tb.x1;
-        NB[k] = (rj + 1 < RW ? 1u : 0u) | (rj > 0 ? 2u : 0u) | (i + RW < nreg ? 4u : 0u) | (ri > 0 ? 8u : 0u);
+        // bits 4+: Manhattan distance to the tile -- the site matters to the tile's
+        // level d + H state only through levels < H - distance (see the level loop)
+        const int dx_ = max(max(tb.x0 - x, x - (tb.x1 - 1)), 0), dy_ = max(max(tb.y0 - y, y - (tb.y1 - 1)), 0);
+        NB[k] = (rj + 1 < RW ? 1u : 0u) | (rj > 0 ? 2u : 0u) | (i + RW < nreg ? 4u : 0u) | (ri > 0 ? 8u : 0u) |
+                ((unsigned)(dx_ + dy_) << 4);
         if (smem_masks(NW) && load_masks && ok) {
 #pragma unroll
             for (int q = 0; q < (PACK ? 7 : 13 * NW); ++q) sM[q * RS + i] = b.mask[(size_t)q * P + c];
@@ -212,7 +216,12 @@ __device__ unsigned bfs_round(const Prob &p, const Arr3 &a, const Bits2 &b, cons
 #pragma unroll
         for (int k = 0; k < SPT; ++k) {
             const int i = threadIdx.x + k * blockDim.x;
-            if (C[k] < 0) continue;
+            // a level moves information at most one site (Manhattan), so the tile's
+            // state after the round's H levels depends on a site at distance r only
+            // through its state after levels < H - r: iteration lev computes the sites
+            // with r <= H - 1 - lev (a shrinking diamond-cornered box; the skipped
+            // halo sites are never read by a computed one)
+            if (C[k] < 0 || (int)(NB[k] >> 4) > H - 1 - lev) continue;
             BW<NW> F, Fn[4];
             uint32_t any = 0u;
 #pragma unroll
@@ -730,6 +739,13 @@ __device__ __forceinline__ void tilesolve_body(PP p, BB b, AA a, const Geo &g, u
                             const bool ovf = s_tn[cur ^ 1] > (unsigned)tail_cap;
                             __syncthreads();
                             if (threadIdx.x == 0) s_tn[cur] = 0u;
+                            if (p.trace > 1 && p.tbuf && threadIdx.x == 0 && pulses < 4096) {   // tail pulses: pulse + 1000
+                                const unsigned long long now = gz2::gtimer();
+                                p.tbuf[2 * pulses] = ((unsigned long long)sweeps << 48) |
+                                                     ((unsigned long long)(1000 + tp) << 32) | (unsigned long long)n;
+                                p.tbuf[2 * pulses + 1] = now - t_pulse;
+                                t_pulse = now;
+                            }
                             parity ^= 1;
                             ++pulses;
                             cur ^= 1;

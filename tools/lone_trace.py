@@ -18,12 +18,25 @@ print('device_ms', r.stats['device_ms'], 'pulses', r.stats['pulses'], r.stats['p
 for seed in sys.argv[1:]:
     p = subprocess.run([sys.executable, "-c", code, seed], capture_output=True, text=True)
     print(f"seed {seed}:", p.stdout.strip().splitlines()[-1] if p.stdout.strip() else p.stderr[-500:])
+    raw = [l for l in p.stderr.splitlines() if l.startswith("gz_pulse")]
+    open(os.path.join(ROOT, "gpurun_out", f"lone_trace_{seed}.raw"), "w").write("\n".join(raw) + "\n")
+    tail = collections.defaultdict(lambda: [0, 0.0, 0])
+    for line in raw:
+        m = re.match(r"gz_pulse sweep (\d+) pulse (\d+) groups (\d+) dt_us ([\d.]+)", line)
+        if m and int(m.group(2)) >= 1000:
+            t = tail[int(m.group(1))]
+            t[0] += 1; t[1] += float(m.group(4)); t[2] += int(m.group(3))
+    for sw in sorted(tail):
+        n, t, g = tail[sw]
+        print(f"  sweep {sw:3d} tail: {n:3d} pulses, {t / 1000:6.3f} ms, {g / max(n, 1):6.1f} groups/pulse")
     buckets = collections.defaultdict(lambda: [0, 0.0, 0])
     for line in p.stderr.splitlines():
         m = re.match(r"gz_pulse sweep (\d+) pulse (\d+) groups (\d+) dt_us ([\d.]+)", line)
         if not m:
             continue
         g, dt = int(m.group(3)), float(m.group(4))
+        if int(m.group(2)) >= 1000:
+            continue
         b = 0 if g == 0 else 1 if g <= 8 else 2 if g <= 64 else 3 if g <= 512 else 4 if g <= 4096 else 5
         buckets[b][0] += 1
         buckets[b][1] += dt
