@@ -97,6 +97,8 @@ __device__ __forceinline__ T gz_atomic_or(const Prob &p, T *a, T v) {
 enum Ctr : int {
     CTR_FLOW = 0, CTR_OFFSET, CTR_PRESAT, CTR_PUSHES, CTR_RELABELS, CTR_ENERGY, CTR_HARDVIOL,
     CTR_SWEEPS, CTR_BFS_PASSES, CTR_REACH_PASSES, CTR_STATUS, CTR_CONVERGED, CTR_STRANDED, CTR_PULSES,
+    CTR_TDRAW = 14,     // batched pair solves: %globaltimer when the pair was drawn (stats rows only)
+    CTR_TEND = 15,      // batched pair solves: %globaltimer when it finished (stats rows only)
     CTR_FLAG0 = 16,     // 3 rotating "changed" flags
     CTR_ACT0 = 20,      // 3 rotating active counters
     CTR_T0 = 24,        // 6 phase timers (ns): init, mask build, bfs, pulses, reach, tail

@@ -811,6 +811,17 @@ struct DevicePool {
         CK(cudaHostGetDevicePointer((void **)&flag_dev, flag_host, 0));
         return GZ_OK;
     }
+    void *scratch = nullptr;   // per-call device scratch of gz_solve_pairs (grow-only)
+    size_t scratch_n = 0;
+    int scratch_ready(size_t n) {
+        if (scratch_n >= n) return GZ_OK;
+        if (scratch) cudaFree(scratch);
+        scratch = nullptr;
+        scratch_n = 0;
+        CK(cudaMalloc(&scratch, n));
+        scratch_n = n;
+        return GZ_OK;
+    }
     int pinned_ready(size_t n) {
         if (pinned_n >= n) return GZ_OK;
         if (pinned) cudaFreeHost(pinned);
@@ -1307,6 +1318,9 @@ int plan_pairs(int rows, int cols, int m, int batch, size_t workspace_bytes, int
 int solve_pairs_batched(const uint8_t *left, const uint8_t *right, int batch, int img_h, int img_w, int channels,
                         const gz_cuboid *cb, const gz_energy *energy, const gz_sched *sched, int32_t *labels_out,
                         gz_stats *stats_out, void *workspace, size_t workspace_bytes, cudaStream_t s, int T) {
+    const auto h_t0 = std::chrono::steady_clock::now();   // (GZ_PAIR_TIMELINE: host phases)
+    auto h_us = [&]() { return (long long)std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() - h_t0).count(); };
+    long long h_launch = 0, h_tail = 0, h_sync = 0;
     const int rows = cb->y_extent, cols = cb->g_extent, m = cb->m, P = rows * cols;
     const size_t one = ws_bytes(rows, cols, m);
     PairsPlan pl;
@@ -1339,13 +1353,21 @@ int solve_pairs_batched(const uint8_t *left, const uint8_t *right, int batch, in
     pb.ws_stride = one;
     pb.bits_bytes = w.bits_bytes;
     pb.labels_out = labels_out;
+    DevicePool *pool = device_pool();
+    if (!pool) return GZ_ERR_CUDA;
+    std::lock_guard<std::mutex> lock(pool->mu);
     unsigned long long *dbuf = nullptr;
     const size_t sbytes = (size_t)batch * gz::CTR_COUNT * 8;
     // tail launch (gz_tilesolve.cuh PairBatch): the last `tail` pairs go to a
     // second launch of T2-CTA teams, issued once the first launch's queue is dry
     const int grid1 = nteams * T, batch1 = batch - tail;
     const size_t tbytes = align_up((size_t)nteams * 4) * 2 + align_up((size_t)(nt2 > 0 ? nt2 : 1) * 4) + 256;
-    CK(cudaMallocAsync((void **)&dbuf, sbytes + 256 + tbytes, s));
+    // per-call device scratch (stats rows, queue, team words) from the pool: a
+    // cudaMallocAsync / cudaFreeAsync pair per call let the stream-ordered pool
+    // trim at the closing synchronize, which stalled the call 0.2-0.9 s now and
+    // then after the kernels were done (tools/pair_timeline.py)
+    if ((rc = pool->scratch_ready(sbytes + 256 + tbytes))) return rc;
+    dbuf = (unsigned long long *)pool->scratch;
     pb.stats = dbuf;
     pb.queue = (unsigned *)((uint8_t *)dbuf + sbytes);
     uint8_t *tb = (uint8_t *)dbuf + sbytes + 256;
@@ -1364,9 +1386,6 @@ int solve_pairs_batched(const uint8_t *left, const uint8_t *right, int batch, in
         Workspace wk = carve((uint8_t *)workspace + (size_t)k * one, rows, cols, m);
         CK(cudaMemsetAsync(wk.ctr, 0, gz::CTR_COUNT * 8, s));
     }
-    DevicePool *pool = device_pool();
-    if (!pool) return GZ_ERR_CUDA;
-    std::lock_guard<std::mutex> lock(pool->mu);
     cudaStream_t s2 = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     if (tail) {
@@ -1381,7 +1400,14 @@ int solve_pairs_batched(const uint8_t *left, const uint8_t *right, int batch, in
     }
     void *args[] = {&p, &bb, &a3, &geo, &pb};
     grid = grid1;
+    const char *tl_path = getenv("GZ_PAIR_TIMELINE");   // debug: per-pair draw / end times, host phases
+    cudaEvent_t tev[4] = {nullptr, nullptr, nullptr, nullptr};
+    if (tl_path)
+        for (auto &e : tev) CK(cudaEventCreate(&e));
+    if (tl_path) CK(cudaEventRecord(tev[0], s));
     CK(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(gz4::BLOCK), args, dyn, s));
+    if (tl_path) CK(cudaEventRecord(tev[1], s));
+    h_launch = h_us();
     gz4::Geo geo2 = geo;
     if (tail) {
         gz4::PairBatch pb2 = pb;
@@ -1402,6 +1428,8 @@ int solve_pairs_batched(const uint8_t *left, const uint8_t *right, int batch, in
         }
         void *args2[] = {&p, &bb, &a3, &geo2, &pb2};
         CK(cudaLaunchKernel(kern, dim3(nt2 * T2), dim3(gz4::BLOCK), args2, dyn, s2));
+        if (tl_path) CK(cudaEventRecord(tev[2], s2));
+        h_tail = h_us();
         CK(cudaEventRecord(ev1, s2));
         CK(cudaStreamWaitEvent(s, ev1, 0));
         cudaEventDestroy(ev0);
@@ -1409,8 +1437,29 @@ int solve_pairs_batched(const uint8_t *left, const uint8_t *right, int batch, in
     }
     if ((rc = pool->pinned_ready((size_t)batch * gz::CTR_COUNT))) return rc;
     CK(cudaMemcpyAsync(pool->pinned, dbuf, sbytes, cudaMemcpyDeviceToHost, s));
-    cudaFreeAsync(dbuf, s);
+    unsigned long long tl[3] = {0ull, 0ull, 0ull};
+    if (tl_path) CK(cudaMemcpyAsync(tl, pb.queue, sizeof(tl), cudaMemcpyDeviceToHost, s));
+    if (tl_path) CK(cudaEventRecord(tev[3], s));
+    const long long h_copy = h_us();
     CK(cudaStreamSynchronize(s));
+    h_sync = h_us();
+    if (tl_path) {
+        if (FILE *fp = fopen(tl_path, "a")) {
+            float k1 = 0.f, k2 = 0.f, k3 = 0.f;
+            cudaEventElapsedTime(&k1, tev[0], tev[1]);
+            if (tail) cudaEventElapsedTime(&k2, tev[0], tev[2]);
+            cudaEventElapsedTime(&k3, tev[0], tev[3]);
+            fprintf(fp, "batch %d batch1 %d T %d T2 %d teams %d tail_teams %d dry %llu tail_start %llu h_launch_us %lld h_tail_us %lld h_copy_us %lld h_sync_us %lld ev_k1_us %d ev_k2_us %d ev_end_us %d\n",
+                    batch, batch1, T, T2, nteams, nt2, tl[1], tl[2], h_launch, h_tail, h_copy, h_sync, (int)(k1 * 1e3f),
+                    (int)(k2 * 1e3f), (int)(k3 * 1e3f));
+            for (int b = 0; b < batch; ++b) {
+                const unsigned long long *h = pool->pinned + (size_t)b * gz::CTR_COUNT;
+                fprintf(fp, "pair %d %llu %llu\n", b, h[CTR_TDRAW], h[CTR_TEND]);
+            }
+            fclose(fp);
+        }
+        for (auto &e : tev) cudaEventDestroy(e);
+    }
     for (int b = 0; b < batch && rc == GZ_OK; ++b) {
         const unsigned long long *h = pool->pinned + (size_t)b * gz::CTR_COUNT;
         rc = stats_from_ctr(h, energy->hard_inhibit ? 1 : 0, 1 << 30, (float)(h[CTR_NS] * 1e-6), b < batch1 ? geo.H : geo2.H,

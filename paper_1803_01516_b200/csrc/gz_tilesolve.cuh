@@ -71,6 +71,12 @@ struct Geo {
 // 48-63.  The value a CTA sees when it observes the flip therefore carries the
 // team's OR.  After barrier k every CTA has read word (k-1) % 3, so rank 0
 // clears it for barrier k+2 (nobody reaches k+2 before rank 0 reaches k+1).
+// Release / acquire half of the team barrier.  fence.acq_rel suffices for the
+// pattern (writes -> bar.sync -> fence -> arrive atomic | observe -> fence ->
+// bar.sync -> reads) and is cheaper than __threadfence's fence.sc (MEMBAR.SC);
+// both also invalidate L1 (CCTL.IVALL), which the plain loads after the barrier rely on.
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 struct Team {
     unsigned long long *bar;   // 3 rotating words of this team
     unsigned long long *abort_flag;   // set when a multi-launch team gives up (spin_ns)
@@ -98,7 +104,7 @@ struct Team {
             const unsigned long long inc = (rank == 0 ? 0x80000000ull - (unsigned long long)(nb - 1) : 1ull) |
                                            ((f & 1u) ? 1ull << 32 : 0ull) | ((f & 2u) ? 1ull << 48 : 0ull);
             unsigned long long *word = bar + k3;
-            if (sys) __threadfence_system(); else __threadfence();
+            if (sys) __threadfence_system(); else fence_acq_rel_gpu();
             unsigned long long cur = 0ull;
             bool aborted = spin_ns && *(volatile unsigned long long *)abort_flag;
             if (!aborted) {
@@ -125,7 +131,7 @@ struct Team {
                 if (aborted) cur = 0ull;
                 else if (rank == 0) bar[(k3 + 2) % 3] = 0ull;
             }
-            if (sys) __threadfence_system(); else __threadfence();
+            if (sys) __threadfence_system(); else fence_acq_rel_gpu();
             s_r3[k3] = (unsigned)(cur >> 32);   // CTAs with flag 0 (low 16) / flag 1 (high 16)
         }
         __syncthreads();
@@ -956,6 +962,9 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_pairs_kernel(const __grid_const
     const Team tm{bar, p.ctr + CTR_ABORT, T, cta, 0, 0ull};
     __shared__ unsigned s_t3[3], s_u3[3];
     __shared__ int s_pair;
+    __shared__ unsigned long long s_tdraw;
+    // timeline words after the two queue counters: u64 [1] queue dry, [2] tail launch start
+    if (pb.tail && blockIdx.x == 0 && threadIdx.x == 0) *(unsigned long long *)(pb.queue + 3) = gz2::gtimer();
     if (threadIdx.x < 3) { s_t3[threadIdx.x] = 0u; s_u3[threadIdx.x] = 0u; }
     __syncthreads();
     int phase = 0;
@@ -964,6 +973,8 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_pairs_kernel(const __grid_const
         // ---- next pair: CTA 0 of the team draws it, the team barrier publishes it ----
         if (cta == 0 && threadIdx.x == 0) {
             const int k = pb.lo + (int)atomicAdd(pb.queue, 1u);
+            s_tdraw = gz2::gtimer();
+            if (k == pb.batch && !pb.tail) *(unsigned long long *)(pb.queue + 2) = s_tdraw;   // queue dry (timeline)
             if (T == 1) s_pair = k;
             else *(volatile int *)&p.ctr[CTR_PAIR] = k;
             if (k >= pb.batch && pb.drained && !*(volatile unsigned *)pb.drained) {
@@ -1013,6 +1024,8 @@ __global__ void __launch_bounds__(BLOCK, OCC) gz_pairs_kernel(const __grid_const
         if (cta == 0 && threadIdx.x < CTR_COUNT) {
             unsigned long long v = ((volatile unsigned long long *)p.ctr)[threadIdx.x];
             if (threadIdx.x == CTR_NS) v = gz2::gtimer() - t0;
+            if (threadIdx.x == CTR_TDRAW) v = s_tdraw;
+            if (threadIdx.x == CTR_TEND) v = gz2::gtimer();
             pb.stats[(size_t)pair * CTR_COUNT + threadIdx.x] = v;
         }
     }

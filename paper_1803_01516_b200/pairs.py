@@ -9,6 +9,7 @@ reference-facing end-to-end call (host buffers in, host labels out).
 from __future__ import annotations
 
 import ctypes as C
+from collections.abc import Sequence
 from typing import Optional
 
 import numpy as np
@@ -32,6 +33,33 @@ def _stats_dict(st: _lib.Stats) -> dict:
         "phase_ms": {k: round(float(v), 4) for k, v in
                      zip(("init", "mask_build", "global_relabel", "pulses", "extract", "tail"), st.ms_phase)},
     }
+
+
+class PairStats(Sequence):
+    """Per-pair stats of one batched call: a read-only sequence of dicts over the
+    C ABI's stats array (already in host memory when the call returns); each
+    pair's dict is built on first access, so a large batch does not pay for
+    Python objects nobody reads."""
+
+    def __init__(self, arr):
+        self._arr = arr
+        self._cache = {}
+
+    def __len__(self) -> int:
+        return len(self._arr)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[k] for k in range(*i.indices(len(self)))]
+        n = len(self._arr)
+        if i < 0:
+            i += n
+        if not 0 <= i < n:
+            raise IndexError("pair index out of range")
+        d = self._cache.get(i)
+        if d is None:
+            d = self._cache[i] = _stats_dict(self._arr[i])
+        return d
 
 
 class PairSolver:
@@ -92,7 +120,7 @@ class PairSolver:
         if rc == _lib.GZ_ERR_CONSISTENCY:
             raise InternalConsistencyError("cut cost != labeling energy")
         _lib.check(rc, "gz_solve_pairs")
-        return labels, [_stats_dict(s) for s in stats]
+        return labels, PairStats(stats)
 
     def solve_host(self, left: np.ndarray, right: np.ndarray, labels: Optional[np.ndarray] = None):
         """Host batch in, host labels out (H2D + solve + D2H in one C-ABI call)."""
@@ -114,7 +142,7 @@ class PairSolver:
         if rc == _lib.GZ_ERR_CONSISTENCY:
             raise InternalConsistencyError("cut cost != labeling energy")
         _lib.check(rc, "gz_solve_pairs_host")
-        return labels, [_stats_dict(s) for s in stats]
+        return labels, PairStats(stats)
 
 
 def solve_pairs(left, right, cuboid: CuboidSpec, params: EnergyParams, rounds_per_sweep: int = 12) -> list[CutResult]:
