@@ -212,7 +212,10 @@ struct TailQ {
 // All shuffles are executed by every lane (uniform control flow).
 template <int LP, int R, bool WIN, bool CG = false, int RW = 0>
 struct Arcs {
-    int r[A_COUNT];
+    // (the 14 residuals are not kept: `pos` has their signs, and an arc's residual
+    // is recomputed from the raw words when it is pushed along -- fewer live
+    // registers through the pulse, whose 64-register batched instance spills)
+    unsigned pos;   // bit j: arc j has residual > 0
     unsigned snk;   // bit j: arc j leads into the sink (arcs into the source have r = 0)
     unsigned adm;   // bit j: arc j admissible (residual > 0 and h(u) = h(target) + 1)
     int best;       // relabel height: 1 + the lowest target height over residual arcs (HINF if none)
@@ -224,20 +227,44 @@ struct Arcs {
 
     // target heights are folded into adm / best as soon as they are known (fewer
     // live registers in w_pulse)
-    __device__ __forceinline__ void finish(const int (&hv)[A_COUNT]) {
+    __device__ __forceinline__ void finish(const int (&r)[A_COUNT], const int (&hv)[A_COUNT]) {
         adm = 0u;
+        pos = 0u;
         best = HINF;
 #pragma unroll
         for (int jj = 0; jj < A_COUNT; ++jj)
             if (r[jj] > 0) {
+                pos |= 1u << jj;
                 const int c = hv[jj] + 1;
                 best = min(best, c);
                 if (h_u == c) adm |= 1u << jj;
             }
     }
 
+    // residual of arc jj, valid when its `pos` bit is set (the conditions that zero
+    // an arc -- missing neighbour, source-side target -- clear that bit)
+    __device__ __forceinline__ int res(const Prob &p, int jj) const {
+        const int P2 = 2 * p.pen, cap = p.hard ? p.hcap : p.inh;
+        switch (jj) {
+        case A_UP: return w_cu;
+        case A_DN: return HINF;
+        case A_SR: return w_ph;
+        case A_SL: return P2 - w_phL;
+        case A_SD: return w_pv;
+        case A_SU: return P2 - w_pvU;
+        case A_UR: return w_dbr_up;
+        case A_UL: return w_darL_up;
+        case A_UD: return w_dbd_up;
+        case A_UU: return w_dadU_up;
+        case A_DR: return cap - w_dar;
+        case A_DL: return cap - w_dbrL;
+        case A_DD: return cap - w_dad;
+        default: return cap - w_dbdU;   // A_DU
+        }
+    }
+
     __device__ __forceinline__ void load(const Prob &p, const Arr3 &a, const Lane<LP, R, WIN, RW> &L) {
-        int hv[A_COUNT];
+        int hv[A_COUNT], r[A_COUNT];
         const int I = L.I;
         const bool v = L.valid;
         w_cu = v ? ldx<CG>(a.cu + I) : 0;
@@ -296,7 +323,7 @@ struct Arcs {
             r[A_DL] = (L.has[1] && !bot) ? cap - w_dbrL : 0; hv[A_DL] = hn_below[1];
             r[A_DD] = (L.has[2] && !bot) ? cap - w_dad : 0; hv[A_DD] = hn_below[2];
             r[A_DU] = (L.has[3] && !bot) ? cap - w_dbdU : 0; hv[A_DU] = hn_below[3];
-            finish(hv);
+            finish(r, hv);
             return;
         }
         snk = 0u;
@@ -316,7 +343,7 @@ struct Arcs {
         SETA(A_DD, L.has[2] ? cap - w_dad : 0, L.has[2] ? L.knb(2, t - 1) : K_SRC, hn_below[2]);
         SETA(A_DU, L.has[3] ? cap - w_dbdU : 0, L.has[3] ? L.knb(3, t - 1) : K_SRC, hn_below[3]);
 #undef SETA
-        finish(hv);
+        finish(r, hv);
     }
 };
 
@@ -471,7 +498,7 @@ __device__ void w_build(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
     if (L.valid && (x0 | x1)) a.e[I] = e;
     uint32_t m[13];
 #pragma unroll
-    for (int q = 0; q < 13; ++q) m[q] = seg_ballot<LP>(L.real && A.r[q] > 0);
+    for (int q = 0; q < 13; ++q) m[q] = seg_ballot<LP>(L.real && ((A.pos >> q) & 1u));
     const uint32_t ex = seg_ballot<LP>(L.real && e > 0);
     if (RW && L.valid && L.j == 0) {
         // window-relative ballots -> the site's absolute words
@@ -562,7 +589,7 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
     const bool live = L.real && hu < HINF;
     // upward chain wave through admissible chain arcs
     const bool adm_up = live && ((A.adm >> A_UP) & 1u);
-    const int x_out = chain_wave<LP>(adm_up ? A.r[A_UP] : 0, adm_up ? max(e, 0) : 0, L.j);
+    const int x_out = chain_wave<LP>(adm_up ? A.w_cu : 0, adm_up ? max(e, 0) : 0, L.j);
     const int x_below = from_below<LP>(x_out);   // every lane shuffles (full mask)
     const int x_in = L.j > 0 ? x_below : 0;
     int cu_new = A.w_cu;
@@ -600,7 +627,7 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
 #define GZ_PAIR(arr, idx, word, delta) do { if (ASYNC) atomicAdd(&a.arr[idx], (delta)); else a.arr[idx] = (word) + (delta); } while (0)
 #pragma unroll
         for (int jj = A_SR; jj <= A_DN; ++jj) {
-            const int d = ((A.adm >> jj) & 1u) ? min(rem, A.r[jj]) : 0;
+            const int d = ((A.adm >> jj) & 1u) ? min(rem, A.res(p, jj)) : 0;
             rem -= d;
             if (d <= 0) continue;
             pushed = true;
