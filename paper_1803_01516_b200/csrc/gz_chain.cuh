@@ -536,7 +536,7 @@ __device__ void w_build(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
 // one pulse on a warp group of chains
 template <int LP, int R, bool WIN, bool ASYNC = false, bool DETPUSH = false, int RW = 0>
 __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base, int nsites, int seg, int parity,
-                        long long &flow, long long &pushes, long long &relabels, uint32_t *dirty,
+                        long long &flow, unsigned &pushes, unsigned &relabels, uint32_t *dirty,
                         const TailQ *tq = nullptr) {
     Lane<LP, R, WIN, RW> L;
     L.init(p, c_base, nsites, seg);
@@ -767,7 +767,7 @@ __device__ void w_pulse(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base
 // (no pushes run in this phase) and heights are written to h2 (commit phase).
 template <int LP, int R, bool WIN, int RW = 0>
 __device__ void w_relabel(const Prob &p, const Arr3 &a, const Bits2 &b, int c_base, int nsites, int seg,
-                          int32_t *h2, long long &relabels) {
+                          int32_t *h2, unsigned &relabels) {
     Lane<LP, R, WIN, RW> L;
     L.init(p, c_base, nsites, seg);
     const uint32_t rl = L.valid ? b.RL[L.bword(p)] : 0u;

@@ -340,13 +340,20 @@ __device__ __forceinline__ void tilesolve_body(PP p, BB b, AA a, const Geo &g, u
 #define TEAM_SYNC() (void)tm.sync_or(0u, phase, s_f3, s_r3)
 #define TEAM_OR(f) tm.sync_or((f), phase, s_f3, s_r3)
 #define TEAM_COUNT(f) tm.sync_count((f), phase, s_f3, s_r3)
-    unsigned long long t_prev = 0, t_acc[6] = {0, 0, 0, 0, 0, 0};
+    // phase timers of thread 0 of rank 0, in shared memory (not 16 registers of every
+    // thread): [0..5] phase sums, [6] last tick, [7] start (the watchdog's clock)
+    __shared__ unsigned long long s_tm[8];
+    unsigned long long *const t_acc = s_tm;
     const bool timer = tm.rank == 0 && threadIdx.x == 0;
-    if (timer) t_prev = gz2::gtimer();
-    const unsigned long long t_start = t_prev;   // (the watchdog's clock; thread 0 of rank 0 only)
-#define TICK(slot) do { if (timer) { unsigned long long t_ = gz2::gtimer(); t_acc[slot] += t_ - t_prev; t_prev = t_; } } while (0)
+    if (timer) {
+        for (int q = 0; q < 6; ++q) s_tm[q] = 0ull;
+        s_tm[6] = s_tm[7] = gz2::gtimer();
+    }
+#define t_start (s_tm[7])
+#define TICK(slot) do { if (timer) { unsigned long long t_ = gz2::gtimer(); t_acc[slot] += t_ - s_tm[6]; s_tm[6] = t_; } } while (0)
 #define FOR_TILES for (int tile = g.t0 + cta; tile < g.t1; tile += ncta)
-    long long flow = 0, offset = 0, presat = 0, pushes = 0, relabels = 0;
+    long long flow = 0;
+    unsigned pushes = 0u, relabels = 0u;   // per thread, flushed to the counters every sweep (32 bits suffice)
     volatile unsigned long long *vctr = p.ctr;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     constexpr int CPW = 32 / LP;
@@ -434,17 +441,18 @@ __device__ __forceinline__ void tilesolve_body(PP p, BB b, AA a, const Geo &g, u
         __syncthreads();                                                                         \
     }
 
+    long long offset = 0, presat = 0;
     FOR_TILES {
         const TileBox tb(p, g, tile);
         for_tile_groups<LP>(p, tb, [&](int cb, int ns) { gz3::w_init<LP, R, WIN, RW>(p, a, cb, ns, flow, offset, presat); });
     }
+    // (published now: no live registers for them through the solve)
+    warp_add_u64(&p.ctr[CTR_OFFSET], offset, p.sys);
+    if (!p.init_only) warp_add_u64(&p.ctr[CTR_PRESAT], presat, p.sys);
     for (int i = ttid; i < bwords; i += tstride) b.IN[band_word(i)] = 1u;   // every site starts dirty
     TEAM_SYNC();
     TICK(0);
-    if (p.init_only) {   // graph export: the state planes now hold the capacities
-        warp_add_u64(&p.ctr[CTR_OFFSET], offset, p.sys);
-        return;
-    }
+    if (p.init_only) return;   // graph export: the state planes now hold the capacities
     int sweeps = 0, levels_total = 0, pulses = 0, parity = 0;
     const uint32_t *v_last = nullptr;   // capped stop: visited words of the final (exhaustive) BFS
     int converged = 1;
@@ -766,6 +774,9 @@ __device__ __forceinline__ void tilesolve_body(PP p, BB b, AA a, const Geo &g, u
         }
         TICK(3);
         ++sweeps;
+        warp_add_u64(&p.ctr[CTR_PUSHES], pushes, p.sys);
+        warp_add_u64(&p.ctr[CTR_RELABELS], relabels, p.sys);
+        pushes = relabels = 0u;
         if (p.trace && threadIdx.x == 0 && tm.rank == 0)
             printf("gz_trace sweep %d levels %d pulses %d t %.3f ms bfs %.3f pulses %.3f\n", sweeps, d, pulses,
                    (gz2::gtimer() - t_start) * 1e-6, t_acc[2] * 1e-6, t_acc[3] * 1e-6);
@@ -838,11 +849,10 @@ __device__ __forceinline__ void tilesolve_body(PP p, BB b, AA a, const Geo &g, u
 #undef TEAM_COUNT
     TICK(5);
 #undef TICK
+#undef t_start
     if (timer)
         for (int q = 0; q < 6; ++q) p.ctr[CTR_T0 + q] = t_acc[q];
     warp_add_u64(&p.ctr[CTR_FLOW], flow, p.sys);
-    warp_add_u64(&p.ctr[CTR_OFFSET], offset, p.sys);
-    warp_add_u64(&p.ctr[CTR_PRESAT], presat, p.sys);
     warp_add_u64(&p.ctr[CTR_PUSHES], pushes, p.sys);
     warp_add_u64(&p.ctr[CTR_RELABELS], relabels, p.sys);
     warp_add_u64(&p.ctr[CTR_ENERGY], energy, p.sys);
