@@ -6,6 +6,6 @@ tag=${1:-r2}
 out=gpurun_out
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches_$tag.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-lone > $out/launches_$tag.log 2>&1
-timeout 1500 ncu --set full --clock-control none --import-source on -k regex:gz_pairs -s 3 -c 1 \
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:gz_pairs -s 6 -c 1 \
     -o $out/prof_$tag -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-lone > $out/prof_$tag.log 2>&1
 ls -la $out/prof_$tag.ncu-rep $out/launches_$tag.csv
