@@ -59,6 +59,7 @@ struct Prob {
     int K;               // pulses per sweep
     int k_tail, tail_after;   // v4: pulses per sweep from sweep `tail_after` on (0 = K)
     int tail_mode;            // v4: hand nearly empty pulse phases to one CTA
+    int tail_ctas;            // v4: tail mode once at most this many CTAs had work (GZ_TAIL_CTAS)
     int async_l;              // v4: > 0 = asynchronous pulses, this many iterations per team barrier
     int wl_dedupe;            // v4 exact: push-time dedupe of worklist entries (GZ_WL_DEDUPE)
     int worklist;             // v4 exact: later pulses of a sweep consume a global worklist (1 on, 0 off, -1 auto)

@@ -1038,6 +1038,8 @@ void setup_prob(Prob &p, const Workspace &w, int rows, int cols, int m, const gz
         p.tail_after = ta ? atoi(ta) : 4;
         const char *tmode = getenv("GZ_TAIL_MODE");
         p.tail_mode = tmode ? atoi(tmode) : 1;
+        const char *tc = getenv("GZ_TAIL_CTAS");
+        p.tail_ctas = tc ? atoi(tc) : 16;
         const char *al = getenv("GZ_ASYNC_L");
         p.async_l = al ? atoi(al) : 0;
         const char *wl = getenv("GZ_WORKLIST");

@@ -695,7 +695,7 @@ __device__ __forceinline__ void tilesolve_body(PP p, BB b, AA a, const Geo &g, u
             ++pulses;
             if (idle) break;
             if (tail_ok && p.async_l == 0 && !p.capped && sweeps >= p.tail_after && pulse + 1 < kp &&
-                (g.nb == 1 ? cta_groups <= p.tail_groups : ((cnt >> 16) == 0u && (cnt & 0xffffu) <= TAIL_CTAS))) {
+                (g.nb == 1 ? cta_groups <= p.tail_groups : ((cnt >> 16) == 0u && (int)(cnt & 0xffffu) <= (p.tail_ctas > 0 ? p.tail_ctas : TAIL_CTAS)))) {
                 // ---- tail mode: the few active groups go to CTA 0, which runs the rest of
                 // the sweep's pulses on a shared-memory worklist with CTA barriers only ----
                 const uint32_t *INn = parity ? a.IN0 : a.IN1;
