@@ -23,6 +23,10 @@ solver = gz.PairSolver(cub, gz.EnergyParams(14, 1023), 288, 384, 3)
 solver.solve(Ld, Rd)
 torch.cuda.synchronize()
 ev, wall = [], []
+if os.environ.get("TL_NOGC"):
+    import gc
+    gc.collect()
+    gc.disable()
 for _ in range(reps):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t = time.perf_counter()
